@@ -1,0 +1,12 @@
+"""B200-native divide-and-combine copula MPL fit (arXiv:1609.05530 hot path).
+
+The product is libparcop_b200.so (CUDA, sm_100a) behind the C-ABI in
+include/parcop_b200.h; this package is its Python mirror of the reference's
+`parcop::` interface (see parcop.py).
+"""
+from .parcop import (  # noqa: F401
+    BASE_SEED, CombinedResult, Context, ConvergenceError, CopulaFamily, CudaError, DataMatrix, DomainError,
+    FitResult, Partition, Precision, PseudoSample, Scheme, asymptotic_variance, combine, default_context,
+    family_from_string, fit, fit_blocks, fit_parallel, normalized_ranks, partition, pseudo_loglik, sample_matrix,
+    validate_data,
+)

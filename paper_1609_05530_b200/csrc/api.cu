@@ -1,0 +1,533 @@
+// The C-ABI (include/parcop_b200.h): context, pointer staging, argument
+// validation with the reference's error semantics, and the pipelines that
+// chain the kernels. No CPU fallback exists: every compute path runs on the
+// device or fails with PCB_E_CUDA.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/parcop_b200.h"
+#include "internal.hpp"
+
+struct pcb_context {
+    pcb::Ctx c;
+};
+
+namespace {
+
+std::string g_create_error;
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// A read-only input that may live on the host: staged into a named buffer.
+template <class T>
+const T* dev_in(pcb::Ctx& c, const T* p, size_t count, const char* name) {
+    if (count == 0) return p;
+    if (is_device_ptr(p)) return p;
+    T* d = c.ws.get_t<T>(std::string("in.") + name, count);
+    PCB_CUDA(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+    return d;
+}
+
+// An output that may live on the host: written to a device buffer, then
+// copied back by finish().
+template <class T>
+struct DevOut {
+    T* user;
+    T* dev;
+    size_t count;
+    bool staged;
+    DevOut(pcb::Ctx& c, T* p, size_t n, const char* name) : user(p), dev(p), count(n), staged(false) {
+        if (p && n && !is_device_ptr(p)) {
+            dev = c.ws.get_t<T>(std::string("out.") + name, n);
+            staged = true;
+        }
+    }
+    void finish(pcb::Ctx& c) {
+        if (staged && count) PCB_CUDA(cudaMemcpyAsync(user, dev, count * sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+    }
+};
+
+template <class F>
+int guarded(pcb_context* ctx, F&& f) {
+    if (!ctx) return PCB_E_INVALID;
+    try {
+        PCB_CUDA(cudaSetDevice(ctx->c.device));
+        f();
+        ctx->c.err.clear();
+        return PCB_OK;
+    } catch (const pcb::Error& e) {
+        ctx->c.err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        ctx->c.err = e.what();
+        return PCB_E_CUDA;
+    }
+}
+
+std::vector<uint64_t> check_offsets(const uint64_t* off, uint64_t n_seg, uint64_t n_rows, uint64_t min_rows) {
+    if (!off) throw pcb::Error(PCB_E_INVALID, "seg_offsets is NULL");
+    if (n_seg < 1) throw pcb::Error(PCB_E_INVALID, "need at least one segment");
+    if (off[0] != 0 || off[n_seg] != n_rows)
+        throw pcb::Error(PCB_E_INVALID, "seg_offsets must start at 0 and end at n_rows");
+    std::vector<uint64_t> v(off, off + n_seg + 1);
+    for (uint64_t m = 0; m < n_seg; ++m) {
+        if (v[m + 1] < v[m]) throw pcb::Error(PCB_E_INVALID, "seg_offsets must be ascending");
+        if (v[m + 1] - v[m] < min_rows)
+            throw pcb::Error(PCB_E_INVALID, "data matrix: need at least 2 rows");  // pseudo_obs.hpp:33
+    }
+    return v;
+}
+
+void check_family(int fam) {
+    if (fam < 0 || fam > 2) throw pcb::Error(PCB_E_INVALID, "family must be 0 (Gaussian), 1 (Frank) or 2 (Gumbel)");
+}
+void check_precision(int p) {
+    if (p != PCB_FP64 && p != PCB_FP32) throw pcb::Error(PCB_E_INVALID, "precision must be PCB_FP64 or PCB_FP32");
+}
+
+bool theta_in_domain(int fam, double t) {  // copula.hpp:47-55
+    if (!std::isfinite(t)) return false;
+    if (fam == 0) return t > -1.0 && t < 1.0;
+    if (fam == 1) return t != 0.0;
+    return t >= 1.0;
+}
+
+__global__ void k_check_unit(const double* u1, const double* u2, uint64_t n, int strict, int* flag) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double a = u1[i], b = u2[i];
+        const bool ok = strict ? (a > 0.0 && a < 1.0 && b > 0.0 && b < 1.0)
+                               : (a >= 0.0 && a <= 1.0 && b >= 0.0 && b <= 1.0);
+        if (!ok) *flag = 1;
+    }
+}
+
+// validate_pseudo_sample (pseudo_obs.hpp:79-88) / clamp_unit (copula.hpp:88-92)
+void check_unit(pcb::Ctx& c, const double* u1, const double* u2, uint64_t n, bool strict) {
+    int* flag = c.ws.get_t<int>("chk.flag", 1);
+    PCB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), c.stream));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256 + 1, 148ull * 16));
+    k_check_unit<<<grid, 256, 0, c.stream>>>(u1, u2, n, strict ? 1 : 0, flag);
+    c.count_launch();
+    int* h = static_cast<int*>(c.host_staging(sizeof(int)));
+    PCB_CUDA(cudaMemcpyAsync(h, flag, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    PCB_CUDA(cudaStreamSynchronize(c.stream));
+    if (*h) {
+        if (strict) throw pcb::Error(PCB_E_DOMAIN, "pseudo sample: values must lie strictly in (0,1)");
+        throw pcb::Error(PCB_E_DOMAIN, "copula argument must lie in [0,1]");
+    }
+}
+
+struct RankBufs {
+    pcb::RankOut r;
+    int32_t* bad;
+};
+
+RankBufs rank_buffers(pcb::Ctx& c, uint64_t n_rows, uint64_t n_seg) {
+    RankBufs b;
+    b.r.r2 = c.ws.get_t<uint32_t>("pipe.r2", 2 * n_rows);
+    b.r.pos = c.ws.get_t<uint32_t>("pipe.pos", 2 * n_rows);
+    b.r.lt = c.ws.get_t<uint32_t>("pipe.lt", 2 * n_rows);
+    b.bad = c.ws.get_t<int32_t>("pipe.bad", n_seg);
+    PCB_CUDA(cudaMemsetAsync(b.bad, 0, n_seg * sizeof(int32_t), c.stream));
+    return b;
+}
+
+void finish_stage_times(pcb::Ctx& c) {
+    PCB_CUDA(cudaEventSynchronize(c.ev[5]));
+    for (int k = 0; k < 5; ++k) {
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, c.ev[k], c.ev[k + 1]) != cudaSuccess) {
+            cudaGetLastError();
+            ms = -1.0f;
+        }
+        c.stage_ms[k] = ms;
+    }
+    c.n_stage = 7;
+}
+
+// raw columns (device) -> ranks -> fit -> variance; records to d_out (device)
+void pipeline_blocks(pcb::Ctx& c, int fam, int prec, const double* d1, const double* d2, uint64_t n_rows,
+                     const std::vector<uint64_t>& off, void* d_out) {
+    const uint64_t K = off.size() - 1;
+    RankBufs rb = rank_buffers(c, n_rows, K);
+    PCB_CUDA(cudaEventRecord(c.ev[0], c.stream));
+    pcb::run_ranks(c, d1, d2, n_rows, off, rb.r, rb.bad);
+    pcb::FitIO io;
+    io.family = fam;
+    io.precision = prec;
+    io.n_rows = n_rows;
+    io.off = off;
+    io.r2 = rb.r.r2;
+    io.pos = rb.r.pos;
+    io.lt = rb.r.lt;
+    io.bad = rb.bad;
+    pcb::run_fit(c, io, d_out);
+    finish_stage_times(c);
+}
+
+}  // namespace
+
+extern "C" {
+
+int pcb_abi_version(void) { return PCB_ABI_VERSION; }
+
+pcb_context* pcb_create(int device) {
+    try {
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0) {
+            cudaGetLastError();
+            g_create_error = "no CUDA device available (the library has no CPU fallback)";
+            return nullptr;
+        }
+        if (device < 0 || device >= count) {
+            g_create_error = "device index out of range";
+            return nullptr;
+        }
+        cudaDeviceProp prop;
+        PCB_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) {
+            g_create_error = std::string("device ") + prop.name + " is not sm_100 (this build targets sm_100a only)";
+            return nullptr;
+        }
+        PCB_CUDA(cudaSetDevice(device));
+        auto* ctx = new pcb_context();
+        ctx->c.device = device;
+        PCB_CUDA(cudaStreamCreateWithFlags(&ctx->c.own_stream, cudaStreamNonBlocking));
+        ctx->c.stream = ctx->c.own_stream;
+        for (auto& ev : ctx->c.ev) PCB_CUDA(cudaEventCreate(&ev));
+        pcb::init_tables();
+        return ctx;
+    } catch (const std::exception& ex) {
+        g_create_error = ex.what();
+        return nullptr;
+    }
+}
+
+void pcb_destroy(pcb_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    ctx->c.ws.release();
+    for (auto& ev : ctx->c.ev)
+        if (ev) cudaEventDestroy(ev);
+    if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
+    if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
+    delete ctx;
+}
+
+const char* pcb_last_error(const pcb_context* ctx) { return ctx ? ctx->c.err.c_str() : g_create_error.c_str(); }
+
+int pcb_set_stream(pcb_context* ctx, void* s) {
+    if (!ctx) return PCB_E_INVALID;
+    ctx->c.stream = s ? static_cast<cudaStream_t>(s) : ctx->c.own_stream;
+    return PCB_OK;
+}
+
+uint64_t pcb_launch_count(const pcb_context* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int pcb_stage_times(const pcb_context* ctx, double* ms, int n) {
+    if (!ctx || !ms) return 0;
+    const int k = std::min(n, ctx->c.n_stage);
+    for (int i = 0; i < k; ++i) ms[i] = ctx->c.stage_ms[i];
+    return k;
+}
+
+int pcb_trim(pcb_context* ctx) {
+    return guarded(ctx, [&] {
+        PCB_CUDA(cudaStreamSynchronize(ctx->c.stream));
+        ctx->c.ws.release();
+    });
+}
+
+int pcb_normalized_ranks(pcb_context* ctx, const double* col1, const double* col2, uint64_t n_rows,
+                         const uint64_t* seg_offsets, uint64_t n_seg, double* u1, double* u2) {
+    return guarded(ctx, [&] {
+        pcb::Ctx& c = ctx->c;
+        if (!col1 || !col2 || !u1 || !u2) throw pcb::Error(PCB_E_INVALID, "NULL column pointer");
+        const auto off = check_offsets(seg_offsets, n_seg, n_rows, 2);
+        const double* d1 = dev_in(c, col1, n_rows, "c1");
+        const double* d2 = dev_in(c, col2, n_rows, "c2");
+        RankBufs rb = rank_buffers(c, n_rows, n_seg);
+        pcb::run_ranks(c, d1, d2, n_rows, off, rb.r, rb.bad);
+        std::vector<int32_t> bad(n_seg);
+        PCB_CUDA(cudaMemcpyAsync(bad.data(), rb.bad, n_seg * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+        for (int32_t b : bad)
+            if (b) throw pcb::Error(PCB_E_DOMAIN, "data matrix: non-finite value");  // pseudo_obs.hpp:36
+        DevOut<double> o1(c, u1, n_rows, "u1"), o2(c, u2, n_rows, "u2");
+        pcb::ranks_to_u(c, rb.r.r2, n_rows, off, o1.dev, o2.dev);
+        o1.finish(c);
+        o2.finish(c);
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int pcb_pseudo_loglik(pcb_context* ctx, int family, const double* theta, const double* u1, const double* u2,
+                      uint64_t n_rows, const uint64_t* seg_offsets, uint64_t n_seg, double* loglik) {
+    return guarded(ctx, [&] {
+        pcb::Ctx& c = ctx->c;
+        check_family(family);
+        if (!theta || !u1 || !u2 || !loglik) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        const auto off = check_offsets(seg_offsets, n_seg, n_rows, 0);
+        std::vector<double> th(n_seg);
+        if (is_device_ptr(theta))
+            PCB_CUDA(cudaMemcpy(th.data(), theta, n_seg * sizeof(double), cudaMemcpyDeviceToHost));
+        else
+            std::memcpy(th.data(), theta, n_seg * sizeof(double));
+        for (double t : th)
+            if (!theta_in_domain(family, t)) throw pcb::Error(PCB_E_DOMAIN, "theta outside the family domain");
+        const double* d1 = dev_in(c, u1, n_rows, "u1");
+        const double* d2 = dev_in(c, u2, n_rows, "u2");
+        check_unit(c, d1, d2, n_rows, false);
+        const double* dth = dev_in(c, theta, n_seg, "theta");
+        DevOut<double> o(c, loglik, n_seg, "loglik");
+        pcb::run_loglik(c, family, dth, d1, d2, off, o.dev);
+        o.finish(c);
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int pcb_fit(pcb_context* ctx, int family, int precision, const double* u1, const double* u2, uint64_t n_rows,
+            const uint64_t* seg_offsets, uint64_t n_seg, pcb_fit_result* out) {
+    return guarded(ctx, [&] {
+        pcb::Ctx& c = ctx->c;
+        check_family(family);
+        check_precision(precision);
+        if (!u1 || !u2 || !out) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        const auto off = check_offsets(seg_offsets, n_seg, n_rows, 0);
+        const double* d1 = dev_in(c, u1, n_rows, "u1");
+        const double* d2 = dev_in(c, u2, n_rows, "u2");
+        check_unit(c, d1, d2, n_rows, true);
+        RankBufs rb = rank_buffers(c, n_rows, n_seg);
+        PCB_CUDA(cudaEventRecord(c.ev[0], c.stream));
+        pcb::run_ranks(c, d1, d2, n_rows, off, rb.r, rb.bad);  // order statistics for the W-term
+        pcb::FitIO io;
+        io.family = family;
+        io.precision = precision;
+        io.n_rows = n_rows;
+        io.off = off;
+        io.u1 = d1;
+        io.u2 = d2;
+        io.pos = rb.r.pos;
+        io.lt = rb.r.lt;
+        DevOut<pcb_fit_result> o(c, out, n_seg, "fit");
+        pcb::run_fit(c, io, o.dev);
+        finish_stage_times(c);
+        o.finish(c);
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int pcb_asymptotic_variance(pcb_context* ctx, int family, const double* theta_hat, const double* u1,
+                            const double* u2, uint64_t n_rows, const uint64_t* seg_offsets, uint64_t n_seg,
+                            double* sigma2) {
+    bool info_bad = false;
+    int rc = guarded(ctx, [&] {
+        pcb::Ctx& c = ctx->c;
+        check_family(family);
+        if (!theta_hat || !u1 || !u2 || !sigma2) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        const auto off = check_offsets(seg_offsets, n_seg, n_rows, 0);
+        std::vector<double> th(n_seg);
+        if (is_device_ptr(theta_hat))
+            PCB_CUDA(cudaMemcpy(th.data(), theta_hat, n_seg * sizeof(double), cudaMemcpyDeviceToHost));
+        else
+            std::memcpy(th.data(), theta_hat, n_seg * sizeof(double));
+        for (double t : th)
+            if (!theta_in_domain(family, t)) throw pcb::Error(PCB_E_DOMAIN, "theta outside the family domain");
+        const double* d1 = dev_in(c, u1, n_rows, "u1");
+        const double* d2 = dev_in(c, u2, n_rows, "u2");
+        check_unit(c, d1, d2, n_rows, true);
+        const double* dth = dev_in(c, theta_hat, n_seg, "theta");
+        RankBufs rb = rank_buffers(c, n_rows, n_seg);
+        PCB_CUDA(cudaEventRecord(c.ev[0], c.stream));
+        pcb::run_ranks(c, d1, d2, n_rows, off, rb.r, rb.bad);
+        pcb::FitIO io;
+        io.family = family;
+        io.n_rows = n_rows;
+        io.off = off;
+        io.u1 = d1;
+        io.u2 = d2;
+        io.pos = rb.r.pos;
+        io.lt = rb.r.lt;
+        io.theta_in = dth;
+        io.do_fit = false;
+        auto* rec = c.ws.get_t<pcb_fit_result>("var.rec", n_seg);
+        pcb::run_fit(c, io, rec);
+        std::vector<pcb_fit_result> h(n_seg);
+        PCB_CUDA(cudaMemcpyAsync(h.data(), rec, n_seg * sizeof(pcb_fit_result), cudaMemcpyDeviceToHost, c.stream));
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+        std::vector<double> s2(n_seg);
+        for (uint64_t m = 0; m < n_seg; ++m) {
+            s2[m] = h[m].sigma2;
+            if (h[m].status == PCB_BLOCK_INFO_NONPOS) info_bad = true;
+        }
+        if (is_device_ptr(sigma2))
+            PCB_CUDA(cudaMemcpy(sigma2, s2.data(), n_seg * sizeof(double), cudaMemcpyHostToDevice));
+        else
+            std::memcpy(sigma2, s2.data(), n_seg * sizeof(double));
+    });
+    if (rc == PCB_OK && info_bad) {
+        ctx->c.err = "asymptotic_variance: information <= 0";
+        return PCB_E_DOMAIN;
+    }
+    return rc;
+}
+
+int pcb_partition(uint64_t n_rows, uint64_t n_blocks, int scheme, uint64_t* offsets) {
+    if (!offsets || n_blocks < 1) return PCB_E_INVALID;
+    if (scheme != PCB_CONTIGUOUS && scheme != PCB_STRIDED) return PCB_E_INVALID;
+    const uint64_t q = n_rows / n_blocks;
+    if (q < 30) return PCB_E_INVALID;
+    if (scheme == PCB_CONTIGUOUS) {
+        for (uint64_t m = 0; m < n_blocks; ++m) offsets[m] = m * q;
+        offsets[n_blocks] = n_rows;
+    } else {
+        const uint64_t rem = n_rows % n_blocks;
+        uint64_t acc = 0;
+        for (uint64_t m = 0; m < n_blocks; ++m) {
+            offsets[m] = acc;
+            acc += q + (m < rem ? 1 : 0);
+        }
+        offsets[n_blocks] = acc;
+    }
+    return PCB_OK;
+}
+
+int pcb_combine(pcb_context* ctx, const pcb_fit_result* results, uint64_t n_blocks, double* weights,
+                pcb_combined* out) {
+    bool none = false;
+    int rc = guarded(ctx, [&] {
+        pcb::Ctx& c = ctx->c;
+        if (!results || !out || n_blocks < 1) throw pcb::Error(PCB_E_INVALID, "combine: empty input");
+        const pcb_fit_result* dr = dev_in(c, results, n_blocks, "comb");
+        DevOut<double> w(c, weights, weights ? n_blocks : 0, "w");
+        double* d3 = c.ws.get_t<double>("comb.out", 3);
+        pcb::run_combine(c, dr, n_blocks, weights ? w.dev : nullptr, d3);
+        double h3[3];
+        PCB_CUDA(cudaMemcpyAsync(h3, d3, sizeof h3, cudaMemcpyDeviceToHost, c.stream));
+        w.finish(c);
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+        pcb_combined r;
+        r.theta_combined = h3[0];
+        r.total_weight = h3[1];
+        r.blocks_used = static_cast<uint64_t>(h3[2]);
+        if (is_device_ptr(out)) PCB_CUDA(cudaMemcpy(out, &r, sizeof r, cudaMemcpyHostToDevice));
+        else *out = r;
+        none = r.blocks_used == 0;
+    });
+    if (rc == PCB_OK && none) {
+        ctx->c.err = "combine: no converged blocks";
+        return PCB_E_CONVERGENCE;
+    }
+    return rc;
+}
+
+int pcb_fit_blocks(pcb_context* ctx, int family, int precision, const double* col1, const double* col2,
+                   uint64_t n_rows, const uint64_t* seg_offsets, uint64_t n_seg, pcb_fit_result* out) {
+    return guarded(ctx, [&] {
+        pcb::Ctx& c = ctx->c;
+        check_family(family);
+        check_precision(precision);
+        if (!col1 || !col2 || !out) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        const auto off = check_offsets(seg_offsets, n_seg, n_rows, 2);
+        const double* d1 = dev_in(c, col1, n_rows, "c1");
+        const double* d2 = dev_in(c, col2, n_rows, "c2");
+        DevOut<pcb_fit_result> o(c, out, n_seg, "fit");
+        pipeline_blocks(c, family, precision, d1, d2, n_rows, off, o.dev);
+        o.finish(c);
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int pcb_fit_parallel(pcb_context* ctx, int family, int precision, const double* col1, const double* col2,
+                     uint64_t n_rows, uint64_t n_blocks, int scheme, pcb_fit_result* per_block, double* weights,
+                     pcb_combined* out) {
+    bool none = false;
+    int rc = guarded(ctx, [&] {
+        pcb::Ctx& c = ctx->c;
+        check_family(family);
+        check_precision(precision);
+        if (!col1 || !col2 || !out) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        std::vector<uint64_t> off(n_blocks + 1);
+        if (n_blocks < 1) throw pcb::Error(PCB_E_INVALID, "partition: need M >= 1");
+        if (pcb_partition(n_rows, n_blocks, scheme, off.data()) != PCB_OK)
+            throw pcb::Error(PCB_E_INVALID, "partition: block below the 30-row floor");
+        const double* d1 = dev_in(c, col1, n_rows, "c1");
+        const double* d2 = dev_in(c, col2, n_rows, "c2");
+        if (scheme == PCB_STRIDED) {
+            double* g1 = c.ws.get_t<double>("strided.c1", n_rows);
+            double* g2 = c.ws.get_t<double>("strided.c2", n_rows);
+            pcb::run_strided_gather(c, d1, n_rows, n_blocks, g1);
+            pcb::run_strided_gather(c, d2, n_rows, n_blocks, g2);
+            d1 = g1;
+            d2 = g2;
+        }
+        auto* rec = c.ws.get_t<pcb_fit_result>("par.rec", n_blocks);
+        pipeline_blocks(c, family, precision, d1, d2, n_rows, off, rec);
+        DevOut<double> w(c, weights, weights ? n_blocks : 0, "w");
+        double* d3 = c.ws.get_t<double>("comb.out", 3);
+        pcb::run_combine(c, rec, n_blocks, weights ? w.dev : nullptr, d3);
+        double h3[3];
+        PCB_CUDA(cudaMemcpyAsync(h3, d3, sizeof h3, cudaMemcpyDeviceToHost, c.stream));
+        w.finish(c);
+        if (per_block) {
+            if (is_device_ptr(per_block))
+                PCB_CUDA(cudaMemcpyAsync(per_block, rec, n_blocks * sizeof(pcb_fit_result), cudaMemcpyDeviceToDevice,
+                                         c.stream));
+            else
+                PCB_CUDA(cudaMemcpyAsync(per_block, rec, n_blocks * sizeof(pcb_fit_result), cudaMemcpyDeviceToHost,
+                                         c.stream));
+        }
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+        out->theta_combined = h3[0];
+        out->total_weight = h3[1];
+        out->blocks_used = static_cast<uint64_t>(h3[2]);
+        none = out->blocks_used == 0;
+    });
+    if (rc == PCB_OK && none) {
+        ctx->c.err = "fit_parallel: all blocks failed";
+        return PCB_E_CONVERGENCE;
+    }
+    return rc;
+}
+
+int pcb_sample(pcb_context* ctx, int family, double theta, uint64_t n_total, uint64_t n_blocks_total,
+               uint64_t first_block, uint64_t last_block, uint64_t base_seed, double* col1, double* col2) {
+    return guarded(ctx, [&] {
+        pcb::Ctx& c = ctx->c;
+        check_family(family);
+        if (!theta_in_domain(family, theta)) throw pcb::Error(PCB_E_DOMAIN, "theta outside the family domain");
+        if (n_blocks_total < 1 || n_total < n_blocks_total || first_block > last_block || last_block > n_blocks_total)
+            throw pcb::Error(PCB_E_INVALID, "sample: bad block range");
+        if (!col1 || !col2) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        const uint64_t q = n_total / n_blocks_total;
+        const uint64_t rows = (last_block == n_blocks_total ? n_total : last_block * q) - first_block * q;
+        DevOut<double> o1(c, col1, rows, "s1"), o2(c, col2, rows, "s2");
+        pcb::run_sample(c, family, theta, n_total, n_blocks_total, first_block, last_block, base_seed, o1.dev, o2.dev);
+        o1.finish(c);
+        o2.finish(c);
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int pcb_measure_fp64_peak(pcb_context* ctx, double* v) {
+    return guarded(ctx, [&] {
+        if (!v) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        *v = pcb::run_fp64_peak(ctx->c);
+    });
+}
+
+}  // extern "C"

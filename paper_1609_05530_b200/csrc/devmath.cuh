@@ -1,0 +1,398 @@
+// Per-point copula arithmetic for sm_100a (device side).
+//
+// Restates the reference formulas (copula.hpp:106-269, normal.hpp:15-81) for
+// the GPU: theta-independent sub-expressions are hoisted out of the point
+// loop (per-block constants in *Theta structs), divisions by per-theta
+// constants become multiplies by hoisted reciprocals, per-point divisions by
+// the same denominator share one reciprocal, and the likelihood passes
+// compute only what Newton needs (score, Hessian). Values agree with the
+// reference to a few ulp per point; parity of the reductions is enforced by
+// tests/test_gpu_parity.py against the CPU oracle.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace pcb {
+
+// ------------------------------------------------------------------ normal
+__device__ __forceinline__ double dev_phi_pdf(double x) {  // normal.hpp:15-18
+    return 0.3989422804014326779399 * exp(-0.5 * x * x);
+}
+
+// Wichura AS241 (normal.hpp:37-81); same coefficients and Horner order.
+__device__ inline double dev_phi_inv(double p) {
+    const double q = p - 0.5;
+    if (fabs(q) <= 0.425) {
+        const double r = 0.180625 - q * q;
+        double n = 2.5090809287301226727e+3;
+        n = n * r + 3.3430575583588128105e+4;
+        n = n * r + 6.7265770927008700853e+4;
+        n = n * r + 4.5921953931549871457e+4;
+        n = n * r + 1.3731693765509461125e+4;
+        n = n * r + 1.9715909503065514427e+3;
+        n = n * r + 1.3314166789178437745e+2;
+        n = n * r + 3.3871328727963666080e+0;
+        double d = 5.2264952788528545610e+3;
+        d = d * r + 2.8729085735721942674e+4;
+        d = d * r + 3.9307895800092710610e+4;
+        d = d * r + 2.1213794301586595867e+4;
+        d = d * r + 5.3941960214247511077e+3;
+        d = d * r + 6.8718700749205790830e+2;
+        d = d * r + 4.2313330701600911252e+1;
+        d = d * r + 1.0;
+        return q * n / d;
+    }
+    double r = sqrt(-log(q < 0.0 ? p : 1.0 - p));
+    double x;
+    if (r <= 5.0) {
+        r -= 1.6;
+        double n = 7.74545014278341407640e-4;
+        n = n * r + 2.27238449892691845833e-2;
+        n = n * r + 2.41780725177450611770e-1;
+        n = n * r + 1.27045825245236838258e+0;
+        n = n * r + 3.64784832476320460504e+0;
+        n = n * r + 5.76949722146069140550e+0;
+        n = n * r + 4.63033784615654529590e+0;
+        n = n * r + 1.42343711074968357734e+0;
+        double d = 1.05075007164441684324e-9;
+        d = d * r + 5.47593808499534494600e-4;
+        d = d * r + 1.51986665636164571966e-2;
+        d = d * r + 1.48103976427480074590e-1;
+        d = d * r + 6.89767334985100004550e-1;
+        d = d * r + 1.67638483018380384940e+0;
+        d = d * r + 2.05319162663775882187e+0;
+        d = d * r + 1.0;
+        x = n / d;
+    } else {
+        r -= 5.0;
+        double n = 2.01033439929228813265e-7;
+        n = n * r + 2.71155556874348757815e-5;
+        n = n * r + 1.24266094738807843860e-3;
+        n = n * r + 2.65321895265761230930e-2;
+        n = n * r + 2.96560571828504891230e-1;
+        n = n * r + 1.78482653991729133580e+0;
+        n = n * r + 5.46378491116411436990e+0;
+        n = n * r + 6.65790464350110377720e+0;
+        double d = 2.04426310338993978564e-15;
+        d = d * r + 1.42151175831644588870e-7;
+        d = d * r + 1.84631831751005468180e-5;
+        d = d * r + 7.86869131145613259100e-4;
+        d = d * r + 1.48753612908506148525e-2;
+        d = d * r + 1.36929880922735805310e-1;
+        d = d * r + 5.99832206555887937690e-1;
+        d = d * r + 1.0;
+        x = n / d;
+    }
+    return q < 0.0 ? -x : x;
+}
+
+__device__ __forceinline__ double clip_log(double v) {  // copula.hpp:94-97
+    if (isnan(v)) return -700.0;
+    return fmin(fmax(v, -700.0), 700.0);
+}
+__device__ __forceinline__ double clamp_unit(double u) {  // copula.hpp:88-92 (domain checked by caller)
+    return fmin(fmax(u, 1e-12), 1.0 - 1e-12);
+}
+
+struct PointFull {
+    double logc, score, hess, cross1, cross2;
+};
+
+// ---------------------------------------------------------------- Gaussian
+struct GaussTheta {  // per-theta constants of copula.hpp:110-127
+    double t, tt, ia, ia2, ia3, half_log_a, c_score_xy, c_hess_xy, c_hess_ss, one_tt;
+    __device__ __forceinline__ explicit GaussTheta(double th) {
+        t = th;
+        tt = th * th;
+        const double a = 1.0 - tt;
+        ia = 1.0 / a;
+        ia2 = ia * ia;
+        ia3 = ia2 * ia;
+        half_log_a = -0.5 * log(a);
+        one_tt = 1.0 + tt;
+        c_score_xy = one_tt;
+        c_hess_xy = 2.0 * th * (3.0 + tt);
+        c_hess_ss = 1.0 + 3.0 * tt;
+    }
+};
+
+__device__ __forceinline__ PointFull gauss_full(double x, double y, const GaussTheta& g) {
+    const double xy = x * y, ss = x * x + y * y;
+    PointFull p;
+    p.logc = g.half_log_a + (2.0 * g.t * xy - g.tt * ss) * (0.5 * g.ia);
+    p.score = g.t * g.ia + (g.one_tt * xy - g.t * ss) * g.ia2;
+    p.hess = g.one_tt * g.ia2 + (g.c_hess_xy * xy - g.c_hess_ss * ss) * g.ia3;
+    // cross_j = ((1+t^2) other - 2 t self) / (a^2 phi(self)); 1/phi(s) = sqrt(2pi) e^{s^2/2}
+    const double k = 2.5066282746310002 * g.ia2;
+    p.cross1 = (g.one_tt * y - 2.0 * g.t * x) * (k * exp(0.5 * x * x));
+    p.cross2 = (g.one_tt * x - 2.0 * g.t * y) * (k * exp(0.5 * y * y));
+    return p;
+}
+
+// Sufficient-statistic form of the Gaussian pseudo-likelihood: with
+// Sxy = sum x*y and Sss = sum (x^2+y^2) over n points,
+//   L(t) = -n/2 log(1-t^2) + (2t Sxy - t^2 Sss) / (2(1-t^2))   (sum of copula.hpp:110-113)
+//   S(t) = n t/a + ((1+t^2) Sxy - t Sss)/a^2                   (sum of :121)
+//   H(t) = n(1+t^2)/a^2 + (2t(3+t^2) Sxy - (1+3t^2) Sss)/a^3   (sum of :122-123)
+__device__ __forceinline__ void gauss_stats_sh(double t, double n, double sxy, double sss, double& S, double& H) {
+    const double tt = t * t, a = 1.0 - tt, ia = 1.0 / a, ia2 = ia * ia;
+    S = n * t * ia + ((1.0 + tt) * sxy - t * sss) * ia2;
+    H = n * (1.0 + tt) * ia2 + (2.0 * t * (3.0 + tt) * sxy - (1.0 + 3.0 * tt) * sss) * ia2 * ia;
+}
+
+// ------------------------------------------------------------------- Frank
+// theta > 0 form (copula.hpp:137-172); negative theta via the reflection
+// c(u,v;-t) = c(u,1-v;t) with score and cross1 negated (copula.hpp:260-264).
+struct FrankTheta {
+    double t, inv_t, g, hconst, logc_const;
+    bool neg;
+    __device__ __forceinline__ explicit FrankTheta(double th) {
+        neg = th < 0.0;
+        t = fabs(th);
+        inv_t = 1.0 / t;
+        const double em = expm1(-t);
+        g = exp(-t) / em;
+        hconst = -inv_t * inv_t + g - g * g;
+        logc_const = log(t) + log(-em);
+    }
+};
+
+// score and Hessian only (the Newton pass), fp64
+__device__ __forceinline__ void frank_sh(double u, double v, const FrankTheta& f, double& s, double& h) {
+    if (f.neg) v = 1.0 - v;
+    const double t = f.t;
+    const double lo = fmin(u, v), hi = fmax(u, v);
+    const double ema = expm1(-t * (1.0 - lo));
+    const double e2 = exp(-t * (hi - lo));
+    const double emb = expm1(-t * lo);
+    const double e1 = 1.0 + ema, e3 = 1.0 + emb;
+    const double b = ema + e2 * emb;
+    const double sum = lo + hi;
+    const double bp = lo - e1 + e2 * (hi - sum * e3);
+    const double bpp = e1 - lo * lo + e2 * (sum * sum * e3 - hi * hi);
+    const double rb = 1.0 / b;
+    const double q = bp * rb;
+    const double sc = f.inv_t - f.g - sum - 2.0 * q;
+    s = f.neg ? -sc : sc;
+    h = f.hconst - 2.0 * (bpp * rb - q * q);
+}
+
+// fp32 per-point arithmetic (likelihood path of configs[3]); the caller
+// accumulates in fp64.
+struct FrankThetaF {
+    float t, inv_t, g, hconst;
+    bool neg;
+    __device__ __forceinline__ explicit FrankThetaF(double th) {
+        neg = th < 0.0;
+        const double tt = fabs(th);
+        const double em = expm1(-tt);
+        const double gd = exp(-tt) / em;
+        t = static_cast<float>(tt);
+        inv_t = static_cast<float>(1.0 / tt);
+        g = static_cast<float>(gd);
+        hconst = static_cast<float>(-1.0 / (tt * tt) + gd - gd * gd);
+    }
+};
+
+// fp32 inputs are radially reflected so that lo + hi <= 1 (Frank is
+// radially symmetric: c(u,v) = c(1-u,1-v)), hence 1-lo >= 1/2 carries no
+// cancellation (SURVEY.md §7 hard part 6).
+__device__ __forceinline__ void frank_sh_f(float u, float v, const FrankThetaF& f, float& s, float& h) {
+    const float t = f.t;
+    const float lo = fminf(u, v), hi = fmaxf(u, v);
+    const float ema = expm1f(-t * (1.0f - lo));
+    const float e2 = expf(-t * (hi - lo));
+    const float emb = expm1f(-t * lo);
+    const float e1 = 1.0f + ema, e3 = 1.0f + emb;
+    const float b = ema + e2 * emb;
+    const float sum = lo + hi;
+    const float bp = lo - e1 + e2 * (hi - sum * e3);
+    const float bpp = e1 - lo * lo + e2 * (sum * sum * e3 - hi * hi);
+    const float rb = 1.0f / b;
+    const float q = bp * rb;
+    s = f.inv_t - f.g - sum - 2.0f * q;
+    h = f.hconst - 2.0f * (bpp * rb - q * q);
+}
+
+// copula.hpp:147-154
+__device__ __forceinline__ double frank_cross_dev(double a, double other, double t, double shift, double rb,
+                                                  double bp, double rb2) {
+    const double em = expm1(-t * other);
+    const double ev = 1.0 + em;
+    const double ea = -t * shift * em;
+    const double dea = shift * ((t * a - 1.0) * em + t * other * ev);
+    return -1.0 - 2.0 * (dea * rb - ea * bp * rb2);
+}
+
+// log c, score, Hessian, cross terms at (u, v) — the variance pass.
+__device__ __forceinline__ PointFull frank_full(double u, double v, const FrankTheta& f) {
+    if (f.neg) v = 1.0 - v;
+    const double t = f.t;
+    const double lo = fmin(u, v), hi = fmax(u, v);
+    const double ema = expm1(-t * (1.0 - lo));
+    const double k2 = -t * (hi - lo);
+    const double e2 = exp(k2);
+    const double emb = expm1(-t * lo);
+    const double e1 = 1.0 + ema, e3 = 1.0 + emb;
+    const double b = ema + e2 * emb;
+    const double sum = lo + hi;
+    const double bp = lo - e1 + e2 * (hi - sum * e3);
+    const double bpp = e1 - lo * lo + e2 * (sum * sum * e3 - hi * hi);
+    const double rb = 1.0 / b;
+    const double q = bp * rb;
+    PointFull p;
+    p.logc = f.logc_const + k2 - 2.0 * log(-b);
+    const double sc = f.inv_t - f.g - (u + v) - 2.0 * q;
+    p.hess = f.hconst - 2.0 * (bpp * rb - q * q);
+    const double rb2 = rb * rb;
+    const double c1 = frank_cross_dev(u, v, t, u <= v ? 1.0 : e2, rb, bp, rb2);
+    const double c2 = frank_cross_dev(v, u, t, v <= u ? 1.0 : e2, rb, bp, rb2);
+    p.score = f.neg ? -sc : sc;
+    p.cross1 = f.neg ? -c1 : c1;
+    p.cross2 = c2;
+    return p;
+}
+
+// ------------------------------------------------------------------ Gumbel
+struct GumbelTheta {  // per-theta constants of copula.hpp:238-254
+    double t, inv_t, inv_t2, inv_t3, c1t;
+    __device__ __forceinline__ explicit GumbelTheta(double th) {
+        t = th;
+        inv_t = 1.0 / th;
+        inv_t2 = inv_t * inv_t;
+        inv_t3 = inv_t2 * inv_t;
+        c1t = inv_t - 2.0;
+    }
+};
+
+// Newton pass from the hoisted theta-independent pair (ln(-ln u), ln(-ln v))
+// (copula.hpp:201-204 computed once per point in the prepare pass).
+__device__ __forceinline__ void gumbel_sh(double lx, double ly, const GumbelTheta& g, double& s, double& h) {
+    const double a = g.t * lx, b = g.t * ly;
+    const bool amax = a >= b;
+    const double m = amax ? a : b;
+    const double lmax = amax ? lx : ly, lmin = amax ? ly : lx;
+    const double e = exp((amax ? b : a) - m);  // the other exponential is exactly 1 (copula.hpp:209-210)
+    const double sden = 1.0 + e;
+    const double rs = 1.0 / sden;
+    const double lnS = m + log(sden);
+    const double w = exp(lnS * g.inv_t);
+    const double r = (lmax + e * lmin) * rs;
+    const double r2 = (lmax * lmax + e * lmin * lmin) * rs;
+    const double rt = r2 - r * r;
+    const double lw_t = r * g.inv_t - lnS * g.inv_t2;
+    const double wt = w * lw_t;
+    const double lw_tt = rt * g.inv_t - 2.0 * r * g.inv_t2 + 2.0 * lnS * g.inv_t3;
+    const double wtt = w * (lw_t * lw_t + lw_tt);
+    const double gg = w + g.t - 1.0;
+    const double rg = 1.0 / gg;
+    const double wt1 = wt + 1.0;
+    s = -wt + lx + ly - lnS * g.inv_t2 + g.c1t * r + wt1 * rg;
+    h = -wtt - 2.0 * r * g.inv_t2 + 2.0 * lnS * g.inv_t3 + g.c1t * rt + (wtt * gg - wt1 * wt1) * rg * rg;
+}
+
+struct GumbelThetaF {
+    float t, inv_t, inv_t2, inv_t3, c1t;
+    __device__ __forceinline__ explicit GumbelThetaF(double th) {
+        t = static_cast<float>(th);
+        inv_t = static_cast<float>(1.0 / th);
+        inv_t2 = static_cast<float>(1.0 / (th * th));
+        inv_t3 = static_cast<float>(1.0 / (th * th * th));
+        c1t = static_cast<float>(1.0 / th - 2.0);
+    }
+};
+
+__device__ __forceinline__ void gumbel_sh_f(float lx, float ly, const GumbelThetaF& g, float& s, float& h) {
+    const float a = g.t * lx, b = g.t * ly;
+    const bool amax = a >= b;
+    const float m = amax ? a : b;
+    const float lmax = amax ? lx : ly, lmin = amax ? ly : lx;
+    const float e = expf((amax ? b : a) - m);
+    const float sden = 1.0f + e;
+    const float rs = 1.0f / sden;
+    const float lnS = m + log1pf(e);
+    const float w = expf(lnS * g.inv_t);
+    const float r = (lmax + e * lmin) * rs;
+    const float r2 = (lmax * lmax + e * lmin * lmin) * rs;
+    const float d = lmax - lmin;  // r2 - r^2 = e d^2 / (1+e)^2, free of cancellation
+    const float rt = e * d * d * rs * rs;
+    (void)r2;
+    const float lw_t = r * g.inv_t - lnS * g.inv_t2;
+    const float wt = w * lw_t;
+    const float lw_tt = rt * g.inv_t - 2.0f * r * g.inv_t2 + 2.0f * lnS * g.inv_t3;
+    const float wtt = w * (lw_t * lw_t + lw_tt);
+    const float gg = w + g.t - 1.0f;
+    const float rg = 1.0f / gg;
+    const float wt1 = wt + 1.0f;
+    s = -wt + lx + ly - lnS * g.inv_t2 + g.c1t * r + wt1 * rg;
+    h = -wtt - 2.0f * r * g.inv_t2 + 2.0f * lnS * g.inv_t3 + g.c1t * rt + (wtt * gg - wt1 * wt1) * rg * rg;
+}
+
+// Full evaluation at (u, v) for the variance pass (copula.hpp:199-254).
+__device__ __forceinline__ PointFull gumbel_full(double u, double v, const GumbelTheta& g) {
+    const double x = -log(u), y = -log(v);
+    const double lx = log(x), ly = log(y);
+    const double a = g.t * lx, b = g.t * ly;
+    const double m = fmax(a, b);
+    const double ea = exp(a - m), eb = exp(b - m);
+    const double sden = ea + eb;
+    const double rs = 1.0 / sden;
+    const double lnS = m + log(sden);
+    const double w = exp(lnS * g.inv_t);
+    const double r = (ea * lx + eb * ly) * rs;
+    const double r2 = (ea * lx * lx + eb * ly * ly) * rs;
+    const double pa = exp(a - lnS) / x, pb = exp(b - lnS) / y;
+    const double rt = r2 - r * r;
+    const double lw_t = r * g.inv_t - lnS * g.inv_t2;
+    const double wt = w * lw_t;
+    const double lw_tt = rt * g.inv_t - 2.0 * r * g.inv_t2 + 2.0 * lnS * g.inv_t3;
+    const double wtt = w * (lw_t * lw_t + lw_tt);
+    const double gg = w + g.t - 1.0;
+    const double rg = 1.0 / gg;
+    const double wt1 = wt + 1.0;
+    PointFull p;
+    p.logc = -w + (g.t - 1.0) * (lx + ly) + (x + y) + g.c1t * lnS + log(gg);
+    p.score = -wt + lx + ly - lnS * g.inv_t2 + g.c1t * r + wt1 * rg;
+    p.hess = -wtt - 2.0 * r * g.inv_t2 + 2.0 * lnS * g.inv_t3 + g.c1t * rt + (wtt * gg - wt1 * wt1) * rg * rg;
+    // copula.hpp:228-236
+    const double rg2 = rg * rg;
+    {
+        const double pt = pa * (lx - r);
+        const double cx = -wt * pa - w * pt + 1.0 / x - 2.0 * pa + (1.0 - 2.0 * g.t) * pt +
+                          ((wt * pa + w * pt) * gg - w * pa * wt1) * rg2;
+        p.cross1 = -cx / u;
+    }
+    {
+        const double pt = pb * (ly - r);
+        const double cy = -wt * pb - w * pt + 1.0 / y - 2.0 * pb + (1.0 - 2.0 * g.t) * pt +
+                          ((wt * pb + w * pt) * gg - w * pb * wt1) * rg2;
+        p.cross2 = -cy / v;
+    }
+    return p;
+}
+
+// log c only (pseudo_loglik API), any family; u, v already clamped.
+__device__ __forceinline__ double logc_any(int fam, double t, double u, double v) {
+    if (fam == 0) {
+        const double x = dev_phi_inv(u), y = dev_phi_inv(v);
+        const double a = 1.0 - t * t;
+        return -0.5 * log(a) + (2.0 * t * x * y - t * t * (x * x + y * y)) / (2.0 * a);
+    }
+    if (fam == 1) {
+        double tt = t;
+        if (t < 0.0) { tt = -t; v = 1.0 - v; }
+        const double lo = fmin(u, v), hi = fmax(u, v);
+        const double k2 = -tt * (hi - lo);
+        const double b = expm1(-tt * (1.0 - lo)) + exp(k2) * expm1(-tt * lo);
+        return log(tt) + log(-expm1(-tt)) + k2 - 2.0 * log(-b);
+    }
+    const double x = -log(u), y = -log(v);
+    const double lx = log(x), ly = log(y);
+    const double a = t * lx, b = t * ly;
+    const double m = fmax(a, b);
+    const double lnS = m + log(exp(a - m) + exp(b - m));
+    const double w = exp(lnS / t);
+    return -w + (t - 1.0) * (lx + ly) + (x + y) + (1.0 / t - 2.0) * lnS + log(w + t - 1.0);
+}
+
+}  // namespace pcb

@@ -1,0 +1,750 @@
+// K2 lik_reduce + batched Newton, K3-K5 asymptotic variance, on sm_100a.
+//
+// Replaces the reference's absent mpl_estimator:
+//   fit                 SPEC.md:216-224, 242-244 — here: every block's root of
+//                       the pseudo-score equation, all blocks in lockstep, one
+//                       fused score+Hessian reduction launch per Newton pass
+//   asymptotic_variance SPEC.md:225-233, 246 — one pass for the per-point
+//                       terms with cross derivatives scattered by stable rank,
+//                       a per-(block, column) suffix scan (the W-term), and a
+//                       final reduction of M-hat
+// Data layout (HBM): the rank stage leaves per column r2/pos/lt u32 arrays
+// ([2][n_rows]); the prepare pass writes the theta-independent per-point
+// pair T (double2 or float2, n_rows) the Newton passes stream:
+//   Gaussian : nothing — the fit reduces to Sxy and Sss (sufficient stats)
+//   Frank    : (u, v)   (fp32: edge-encoded, see frank_edge)
+//   Gumbel   : (ln(-ln u), ln(-ln v))   (copula.hpp:201-204, hoisted)
+// Reductions are deterministic: fixed tiles (never straddling a block),
+// fixed per-tile trees, and the last-arriving tile of a block sums the tile
+// partials in tile order — no floating-point atomics anywhere, so results do
+// not depend on scheduling, on the number of GPUs, or on the run.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "devmath.cuh"
+#include "internal.hpp"
+
+namespace pcb {
+namespace {
+
+constexpr int FT = 256;        // threads per fit block
+constexpr int PPT = 8;         // points per thread per tile
+constexpr uint32_t FTILE = FT * PPT;
+constexpr int kMaxPasses = 64;
+constexpr double kTol64 = 2e-8;  // Newton step tolerance (relative); error after ~C*tol^2
+constexpr double kTol32 = 1e-6;
+
+// Spearman-rho -> theta inversion tables for the Archimedean init.
+constexpr int NTAB = 256;
+__constant__ double c_frank_rho[NTAB], c_frank_theta[NTAB];
+__constant__ double c_gumbel_rho[NTAB], c_gumbel_theta[NTAB];
+
+__device__ double invert_table(const double* rho, const double* th, double r) {
+    if (r <= rho[0]) return th[0];
+    if (r >= rho[NTAB - 1]) return th[NTAB - 1];
+    int lo = 0, hi = NTAB - 1;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (rho[mid] <= r) lo = mid;
+        else hi = mid;
+    }
+    const double w = (r - rho[lo]) / (rho[hi] - rho[lo]);
+    return th[lo] + w * (th[hi] - th[lo]);
+}
+
+// Safeguarded Newton step on the pseudo-score (mirrors oracle/mpl_driver.hpp
+// Driver::fit's bracket / boundary rules; SPEC.md:242 keeps iterates inside
+// the domain). Runs in one thread per block.
+__device__ void newton_update(BlockState& s, int fam, double S, double H, double tol, unsigned* running) {
+    s.iters += 1;
+    s.S = S;
+    s.H = H;
+    double t = s.theta;
+    if (!isfinite(S) || !isfinite(H)) {
+        s.status = kNotConverged;
+        atomicSub(running, 1u);
+        return;
+    }
+    if (S > 0.0) s.lo = t;
+    else s.hi = t;
+    if (fam == kGumbel && t == 1.0) {  // boundary theta = 1
+        s.tried_one = 1;
+        if (S <= 0.0) {
+            s.step = 0.0;
+            s.status = kConverged;
+            atomicSub(running, 1u);
+            return;
+        }
+    }
+    double cand = NAN;
+    if (H < 0.0) {
+        cand = t - S / H;
+        if (fabs(cand - t) <= tol * fmax(1.0, fabs(t))) {
+            if (!(fam == kGumbel && cand < 1.0)) t = cand;
+            s.step = cand - s.theta;
+            s.theta = t;
+            s.status = kConverged;
+            atomicSub(running, 1u);
+            return;
+        }
+    }
+    bool inside = isfinite(cand) && cand > s.lo && cand < s.hi;
+    if (!inside && fam == kGumbel && !s.tried_one && isfinite(cand) && cand <= 1.0) {
+        cand = 1.0;
+        inside = true;
+    }
+    if (!inside) {
+        if (isfinite(s.lo) && isfinite(s.hi)) cand = 0.5 * (s.lo + s.hi);
+        else if (isfinite(s.lo)) cand = s.lo + fmax(1.0, fabs(s.lo));
+        else cand = s.hi - fmax(1.0, fabs(s.hi));
+        if (fam == kGumbel && !(cand > 1.0)) cand = 1.0;
+    }
+    if (fam == kFrank && fabs(cand) < 1e-6) cand = cand < 0.0 ? -1e-6 : 1e-6;
+    s.step = cand - t;
+    s.theta = cand;
+    if (fabs(s.step) <= 1e-14 * fmax(1.0, fabs(cand))) {
+        s.status = kConverged;
+        atomicSub(running, 1u);
+        return;
+    }
+    if (s.iters >= kMaxPasses) {
+        s.status = kNotConverged;
+        atomicSub(running, 1u);
+    }
+}
+
+__device__ __forceinline__ void point_u(const uint32_t* r2, const double* u1, const double* u2, uint64_t n_rows,
+                                        uint64_t row, double scale, double& u, double& v) {
+    if (r2) {  // exactly normalized_rank_column's value (pseudo_obs.hpp:59-60)
+        u = __dmul_rn(0.5 * static_cast<double>(r2[row]), scale);
+        v = __dmul_rn(0.5 * static_cast<double>(r2[n_rows + row]), scale);
+    } else {
+        u = u1[row];
+        v = u2[row];
+    }
+}
+
+// Edge encoding for fp32 Frank inputs: p = u (u <= 1/2) or -(1-u) (u > 1/2),
+// computed in fp64, so both u and 1-u keep full fp32 relative precision.
+__device__ __forceinline__ float frank_edge(double u) {
+    return static_cast<float>(u <= 0.5 ? u : -(1.0 - u));
+}
+__device__ __forceinline__ void frank_unedge(float p, float& val, float& comp) {
+    if (p >= 0.0f) {
+        val = p;
+        comp = 1.0f - p;
+    } else {
+        val = 1.0f + p;
+        comp = -p;
+    }
+}
+
+// Last-tile-of-block reduction helper: stores this tile's NV partials; the
+// block's last tile sums all its tiles' partials in tile order.
+template <int NV>
+__device__ bool tile_reduce(double (&v)[NV], double* sh, double* partials, unsigned* tickets, const Seg& S, int m,
+                            uint32_t tile) {
+    block_sum<NV>(v, sh);
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) partials[static_cast<size_t>(tile) * NV + k] = v[k];
+        __threadfence();
+        const uint32_t nt = (S.n + FTILE - 1) / FTILE;
+        const unsigned ticket = atomicAdd(tickets + m, 1u);
+        s_last = ticket == nt - 1;
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    const uint32_t nt = (S.n + FTILE - 1) / FTILE;
+    double acc[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+    for (uint32_t q = threadIdx.x; q < nt; q += FT) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] += __ldcg(partials + static_cast<size_t>(S.tile0 + q) * NV + k);
+    }
+    block_sum<NV>(acc, sh);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = acc[k];
+    if (threadIdx.x == 0) tickets[m] = 0u;
+    return true;
+}
+
+__global__ void k_init_state(BlockState* st, const Seg* segs, int nseg, const int32_t* bad, unsigned* running,
+                             const double* theta_in) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= nseg) return;
+    BlockState s;
+    memset(&s, 0, sizeof s);
+    s.begin = segs[m].begin;
+    s.n = segs[m].n;
+    s.theta = theta_in ? theta_in[m] : NAN;
+    s.lo = -INFINITY;
+    s.hi = INFINITY;
+    s.loglik = NAN;
+    s.sigma2 = NAN;
+    if (bad && bad[m]) s.status = kBadData;
+    else if (s.n < static_cast<uint64_t>(kMinRows)) s.status = kTooSmall;
+    else {
+        s.status = theta_in ? kConverged : kRunning;
+        if (!theta_in) atomicAdd(running, 1u);
+    }
+    st[m] = s;
+}
+
+// Prepare pass: theta-independent per-point pair + init statistics; the
+// block's last tile computes the starting theta (Gaussian: solves the fit).
+template <int FAM, class TO>
+__global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs, int nseg, const uint32_t* r2,
+                                               const double* u1, const double* u2, uint64_t n_rows, TO* T,
+                                               double* partials, unsigned* tickets, unsigned* running, int fp32) {
+    const uint32_t tile = blockIdx.x;
+    const int m = seg_of_tile(segs, nseg, tile);
+    const Seg S = segs[m];
+    if (st[m].status != kRunning) return;
+    const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);
+    const uint32_t base = (tile - S.tile0) * FTILE;
+    double v[2] = {0.0, 0.0};
+#pragma unroll 2
+    for (int k = 0; k < PPT; ++k) {
+        const uint32_t i = base + k * FT + threadIdx.x;
+        if (i >= S.n) break;
+        const uint64_t row = S.begin + i;
+        double u, w;
+        point_u(r2, u1, u2, n_rows, row, scale, u, w);
+        if (FAM == kGaussian) {
+            const double x = dev_phi_inv(clamp_unit(u)), y = dev_phi_inv(clamp_unit(w));
+            v[0] += x * y;
+            v[1] += x * x + y * y;
+        } else {
+            v[0] += u * w;
+            if (FAM == kFrank) {
+                if (sizeof(TO) == 8) T[row] = TO{static_cast<decltype(TO::x)>(frank_edge(u)),
+                                                 static_cast<decltype(TO::x)>(frank_edge(w))};
+                else T[row] = TO{static_cast<decltype(TO::x)>(u), static_cast<decltype(TO::x)>(w)};
+            } else {
+                const double lx = log(-log(clamp_unit(u))), ly = log(-log(clamp_unit(w)));
+                T[row] = TO{static_cast<decltype(TO::x)>(lx), static_cast<decltype(TO::x)>(ly)};
+            }
+        }
+    }
+    __shared__ double sh[(FT / 32) * 2];
+    if (!tile_reduce<2>(v, sh, partials, tickets, S, m, tile)) return;
+    if (threadIdx.x != 0) return;
+    BlockState s = st[m];
+    const double n = static_cast<double>(S.n);
+    s.stat0 = v[0];
+    s.stat1 = v[1];
+    if (FAM == kGaussian) {
+        // Newton on the closed-form S(t), H(t) of the sufficient statistics
+        double t = fmin(fmax(v[0] / (0.5 * v[1]), -0.99), 0.99);
+        double lo = -1.0, hi = 1.0;
+        bool conv = false;
+        for (int it = 0; it < 200; ++it) {
+            double Sg, Hg;
+            gauss_stats_sh(t, n, v[0], v[1], Sg, Hg);
+            if (!isfinite(Sg) || !isfinite(Hg)) break;
+            if (Sg > 0.0) lo = t;
+            else hi = t;
+            double cand = NAN;
+            if (Hg < 0.0) {
+                cand = t - Sg / Hg;
+                if (fabs(cand - t) <= 1e-15 * fmax(1.0, fabs(t))) {
+                    t = cand;
+                    conv = true;
+                    break;
+                }
+            }
+            if (!(isfinite(cand) && cand > lo && cand < hi)) cand = 0.5 * (lo + hi);
+            if (fabs(cand - t) <= 1e-15 * fmax(1.0, fabs(t))) {
+                t = cand;
+                conv = true;
+                break;
+            }
+            t = cand;
+        }
+        s.theta = t;
+        s.iters = 1;
+        s.status = conv ? kConverged : kNotConverged;
+        atomicSub(running, 1u);
+    } else {
+        // Spearman's rho from the pseudo-observations (no-ties form), inverted
+        // through the family's rho(theta) table: a consistent start whose
+        // error is O(n^-1/2), so Newton needs ~3 passes.
+        const double rho = 12.0 * (n + 1.0) / (n - 1.0) * (v[0] / n - 0.25);
+        double t;
+        if (FAM == kFrank) {
+            t = invert_table(c_frank_rho, c_frank_theta, fabs(rho));
+            t = fmax(t, 0.05);
+            if (rho < 0.0) t = -t;
+        } else {
+            t = rho <= 0.0 ? 1.0 : invert_table(c_gumbel_rho, c_gumbel_theta, rho);
+            t = fmax(t, 1.0);
+        }
+        s.theta = t;
+        s.lo = FAM == kGumbel ? 1.0 : -INFINITY;
+        s.hi = INFINITY;
+    }
+    st[m] = s;
+}
+
+// One Newton pass: fused per-point score + Hessian at each running block's
+// current theta, deterministic block reduction, in-kernel Newton update.
+template <int FAM, class TI>
+__global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int nseg, const TI* __restrict__ T,
+                                           double* partials, unsigned* tickets, unsigned* running) {
+    const uint32_t tile = blockIdx.x;
+    const int m = seg_of_tile(segs, nseg, tile);
+    const Seg S = segs[m];
+    if (st[m].status != kRunning) return;
+    const double theta = st[m].theta;
+    const uint32_t base = (tile - S.tile0) * FTILE;
+    const TI* Tb = T + S.begin + base;
+    const uint32_t cnt = min(FTILE, S.n - base);
+    double v[2] = {0.0, 0.0};
+    if (sizeof(TI) == 16) {  // fp64
+        if (FAM == kFrank) {
+            const FrankTheta f(theta);
+#pragma unroll 4
+            for (int k = 0; k < PPT; ++k) {
+                const uint32_t i = k * FT + threadIdx.x;
+                if (i < cnt) {
+                    const TI p = Tb[i];
+                    double s, h;
+                    frank_sh(p.x, p.y, f, s, h);
+                    v[0] += s;
+                    v[1] += h;
+                }
+            }
+        } else {
+            const GumbelTheta g(theta);
+#pragma unroll 4
+            for (int k = 0; k < PPT; ++k) {
+                const uint32_t i = k * FT + threadIdx.x;
+                if (i < cnt) {
+                    const TI p = Tb[i];
+                    double s, h;
+                    gumbel_sh(p.x, p.y, g, s, h);
+                    v[0] += s;
+                    v[1] += h;
+                }
+            }
+        }
+    } else {  // fp32 per-point arithmetic, fp64 accumulation
+        if (FAM == kFrank) {
+            const FrankThetaF f(theta);
+#pragma unroll 4
+            for (int k = 0; k < PPT; ++k) {
+                const uint32_t i = k * FT + threadIdx.x;
+                if (i < cnt) {
+                    const TI p = Tb[i];
+                    float uv, uc, vv, vc;
+                    frank_unedge(p.x, uv, uc);
+                    frank_unedge(p.y, vv, vc);
+                    if (f.neg) {  // c(u,v;-t) = c(u,1-v;t)
+                        const float tmp = vv;
+                        vv = vc;
+                        vc = tmp;
+                    }
+                    // radial symmetry c(u,v) = c(1-u,1-v): evaluate on the side with lo + hi <= 1
+                    if (uv + vv > 1.0f) {
+                        float tmp = uv;
+                        uv = uc;
+                        uc = tmp;
+                        tmp = vv;
+                        vv = vc;
+                        vc = tmp;
+                    }
+                    float s, h;
+                    frank_sh_f(uv, vv, f, s, h);
+                    v[0] += static_cast<double>(f.neg ? -s : s);
+                    v[1] += static_cast<double>(h);
+                }
+            }
+        } else {
+            const GumbelThetaF g(theta);
+#pragma unroll 4
+            for (int k = 0; k < PPT; ++k) {
+                const uint32_t i = k * FT + threadIdx.x;
+                if (i < cnt) {
+                    const TI p = Tb[i];
+                    float s, h;
+                    gumbel_sh_f(p.x, p.y, g, s, h);
+                    v[0] += static_cast<double>(s);
+                    v[1] += static_cast<double>(h);
+                }
+            }
+        }
+    }
+    __shared__ double sh[(FT / 32) * 2];
+    if (!tile_reduce<2>(v, sh, partials, tickets, S, m, tile)) return;
+    if (threadIdx.x == 0) {
+        BlockState s = st[m];
+        newton_update(s, FAM, v[0], v[1], sizeof(TI) == 16 ? kTol64 : kTol32, running);
+        st[m] = s;
+    }
+}
+
+// Variance pass 1 at theta-hat: log c, score, Hessian, cross terms; the
+// cross terms are scattered to their block's stable sorted positions.
+template <int FAM>
+__global__ void __launch_bounds__(FT) k_var_terms(BlockState* st, const Seg* segs, int nseg, const uint32_t* r2,
+                                                 const double* u1, const double* u2, const uint32_t* pos,
+                                                 uint64_t n_rows, double* score, double* A, double* partials,
+                                                 unsigned* tickets) {
+    const uint32_t tile = blockIdx.x;
+    const int m = seg_of_tile(segs, nseg, tile);
+    const Seg S = segs[m];
+    const int32_t status = st[m].status;
+    if (status != kConverged) return;
+    const double theta = st[m].theta;
+    const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);
+    const uint32_t base = (tile - S.tile0) * FTILE;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < PPT; ++k) {
+        const uint32_t i = base + k * FT + threadIdx.x;
+        if (i >= S.n) break;
+        const uint64_t row = S.begin + i;
+        double u, w;
+        point_u(r2, u1, u2, n_rows, row, scale, u, w);
+        u = clamp_unit(u);
+        w = clamp_unit(w);
+        PointFull p;
+        if (FAM == kGaussian) p = gauss_full(dev_phi_inv(u), dev_phi_inv(w), GaussTheta(theta));
+        else if (FAM == kFrank) p = frank_full(u, w, FrankTheta(theta));
+        else p = gumbel_full(u, w, GumbelTheta(theta));
+        score[row] = p.score;
+        A[S.begin + pos[row]] = p.cross1;
+        A[n_rows + S.begin + pos[n_rows + row]] = p.cross2;
+        v[0] += p.hess;
+        v[1] += u * p.cross1;
+        v[2] += w * p.cross2;
+        v[3] += clip_log(p.logc);
+    }
+    __shared__ double sh[(FT / 32) * 4];
+    if (!tile_reduce<4>(v, sh, partials, tickets, S, m, tile)) return;
+    if (threadIdx.x == 0) {
+        st[m].info_sum = v[0];
+        st[m].c1 = v[1];
+        st[m].c2 = v[2];
+        st[m].loglik = v[3];
+    }
+}
+
+// In-place inclusive suffix sum of A over each (block, column) segment; one
+// CTA per segment, fixed chunking (deterministic).
+__global__ void __launch_bounds__(1024) k_suffix(const BlockState* st, const Seg* segs, int nseg, uint64_t n_rows,
+                                                double* A) {
+    const int m = blockIdx.x % nseg;
+    const int col = blockIdx.x / nseg;
+    if (st[m].status != kConverged) return;
+    const Seg S = segs[m];
+    double* a = A + static_cast<uint64_t>(col) * n_rows + S.begin;
+    const uint32_t n = S.n;
+    const uint32_t chunk = (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = min(n, threadIdx.x * chunk), b1 = min(n, b0 + chunk);
+    double local = 0.0;
+    for (uint32_t q = b1; q-- > b0;) local += a[q];
+    // exclusive suffix scan of the chunk totals (chunks to the right)
+    __shared__ double s_tot[1024];
+    s_tot[threadIdx.x] = local;
+    __syncthreads();
+    // Hillis-Steele suffix scan in shared memory (fixed order)
+    for (int o = 1; o < static_cast<int>(blockDim.x); o <<= 1) {
+        double add = 0.0;
+        if (threadIdx.x + o < blockDim.x) add = s_tot[threadIdx.x + o];
+        __syncthreads();
+        s_tot[threadIdx.x] += add;
+        __syncthreads();
+    }
+    double run = threadIdx.x + 1 < blockDim.x ? s_tot[threadIdx.x + 1] : 0.0;
+    for (uint32_t q = b1; q-- > b0;) {
+        run += a[q];
+        a[q] = run;
+    }
+}
+
+// Variance pass 2: W_ji = (suffix at the tie run's first position - C_j)/n,
+// M-hat = mean (score + W_1 + W_2)^2, sigma2 = M/I^2/n.
+__global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* segs, int nseg, const uint32_t* lt,
+                                                 uint64_t n_rows, const double* score, const double* A,
+                                                 double* partials, unsigned* tickets) {
+    const uint32_t tile = blockIdx.x;
+    const int m = seg_of_tile(segs, nseg, tile);
+    const Seg S = segs[m];
+    if (st[m].status != kConverged) return;
+    const double n = static_cast<double>(S.n);
+    const double c1 = st[m].c1, c2 = st[m].c2;
+    const uint32_t base = (tile - S.tile0) * FTILE;
+    double v[1] = {0.0};
+    for (int k = 0; k < PPT; ++k) {
+        const uint32_t i = base + k * FT + threadIdx.x;
+        if (i >= S.n) break;
+        const uint64_t row = S.begin + i;
+        const double w1 = (A[S.begin + lt[row]] - c1) / n;
+        const double w2 = (A[n_rows + S.begin + lt[n_rows + row]] - c2) / n;
+        const double z = score[row] + w1 + w2;
+        v[0] += z * z;
+    }
+    __shared__ double sh[FT / 32];
+    if (!tile_reduce<1>(v, sh, partials, tickets, S, m, tile)) return;
+    if (threadIdx.x == 0) {
+        BlockState s = st[m];
+        const double info = -s.info_sum / n;
+        if (!(info > 0.0)) {
+            s.status = kInfoNonPos;
+            s.sigma2 = NAN;
+        } else {
+            const double mhat = v[0] / n;
+            s.sigma2 = mhat / (info * info) / n;
+        }
+        st[m] = s;
+    }
+}
+
+struct RecordOut {  // == pcb_fit_result
+    double theta_hat, sigma2, loglik;
+    uint64_t n;
+    int32_t iterations, converged, status, reserved;
+};
+
+__global__ void k_finalize(const BlockState* st, int nseg, RecordOut* out, int with_variance) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= nseg) return;
+    const BlockState s = st[m];
+    RecordOut r;
+    r.theta_hat = (s.status == kBadData || s.status == kTooSmall) ? NAN : s.theta;
+    r.sigma2 = with_variance ? s.sigma2 : NAN;
+    r.loglik = s.loglik;
+    r.n = s.n;
+    r.iterations = s.iters;
+    r.converged = s.status == kConverged ? 1 : 0;
+    r.status = s.status == kRunning ? kNotConverged : s.status;
+    r.reserved = 0;
+    out[m] = r;
+}
+
+__global__ void __launch_bounds__(FT) k_loglik(const Seg* segs, int nseg, const double* theta, const double* u1,
+                                              const double* u2, int fam, double* partials, unsigned* tickets,
+                                              double* out) {
+    const uint32_t tile = blockIdx.x;
+    const int m = seg_of_tile(segs, nseg, tile);
+    const Seg S = segs[m];
+    const double t = theta[m];
+    const uint32_t base = (tile - S.tile0) * FTILE;
+    double v[1] = {0.0};
+    for (int k = 0; k < PPT; ++k) {
+        const uint32_t i = base + k * FT + threadIdx.x;
+        if (i >= S.n) break;
+        const uint64_t row = S.begin + i;
+        v[0] += clip_log(logc_any(fam, t, clamp_unit(u1[row]), clamp_unit(u2[row])));
+    }
+    __shared__ double sh[FT / 32];
+    if (!tile_reduce<1>(v, sh, partials, tickets, S, m, tile)) return;
+    if (threadIdx.x == 0) out[m] = v[0];
+}
+
+// ------------------------------------------------------------ host tables
+double debye(int k, double x) {  // D_k(x) = k/x^k int_0^x t^k/(e^t-1) dt, composite Simpson
+    if (x == 0.0) return 1.0;
+    const int N = 2000;
+    const double h = x / N;
+    auto f = [k](double t) { return t == 0.0 ? (k == 1 ? 1.0 : 0.0) : std::pow(t, k) / std::expm1(t); };
+    double s = f(0.0) + f(x);
+    for (int i = 1; i < N; ++i) s += (i & 1 ? 4.0 : 2.0) * f(i * h);
+    return k / std::pow(x, k) * s * h / 3.0;
+}
+
+bool g_tables_ready = false;
+double h_frank_rho[NTAB], h_frank_theta[NTAB], h_gumbel_rho[NTAB], h_gumbel_theta[NTAB];
+
+void build_tables() {
+    if (g_tables_ready) return;
+    // Frank: rho_S(theta) = 1 - 12/theta (D1(theta) - D2(theta)), theta > 0
+    for (int k = 0; k < NTAB; ++k) {
+        const double th = 0.02 + 80.0 * std::pow(static_cast<double>(k) / (NTAB - 1), 2.0);
+        h_frank_theta[k] = th;
+        h_frank_rho[k] = 1.0 - 12.0 / th * (debye(1, th) - debye(2, th));
+    }
+    // Gumbel: rho_S(theta) = 12 int int C(u,v) du dv - 3 by tensor Gauss-Legendre
+    const int Q = 64;
+    std::vector<double> xn(Q), wn(Q);
+    for (int i = 0; i < Q; ++i) {  // Legendre nodes by Newton on P_Q
+        double x = std::cos(M_PI * (i + 0.75) / (Q + 0.5)), dp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = x;
+            for (int j = 2; j <= Q; ++j) {
+                const double p2 = ((2.0 * j - 1.0) * x * p1 - (j - 1.0) * p0) / j;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = Q * (x * p1 - p0) / (x * x - 1.0);
+            const double dx = p1 / dp;
+            x -= dx;
+            if (std::fabs(dx) < 1e-15) break;
+        }
+        xn[i] = 0.5 * (x + 1.0);
+        wn[i] = 1.0 / ((1.0 - x * x) * dp * dp);  // = 0.5 * 2/((1-x^2)P'^2)
+    }
+    for (int k = 0; k < NTAB; ++k) {
+        const double tau = 0.97 * static_cast<double>(k) / (NTAB - 1);
+        const double th = 1.0 / (1.0 - tau);
+        double s = 0.0;
+        for (int i = 0; i < Q; ++i)
+            for (int j = 0; j < Q; ++j) {
+                const double x = -std::log(xn[i]), y = -std::log(xn[j]);
+                s += wn[i] * wn[j] * std::exp(-std::pow(std::pow(x, th) + std::pow(y, th), 1.0 / th));
+            }
+        h_gumbel_theta[k] = th;
+        h_gumbel_rho[k] = 12.0 * s - 3.0;
+    }
+    g_tables_ready = true;
+}
+
+uint32_t ftiles(uint64_t n) { return static_cast<uint32_t>((n + FTILE - 1) / FTILE); }
+
+template <int FAM>
+void launch_prepare(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, const FitIO& io, void* T,
+                    double* part, unsigned* tick, unsigned* running) {
+    if (io.precision == 1 && FAM != kGaussian)
+        k_prepare<FAM, float2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.r2, io.u1, io.u2, io.n_rows,
+                                                          static_cast<float2*>(T), part, tick, running, 1);
+    else
+        k_prepare<FAM, double2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.r2, io.u1, io.u2, io.n_rows,
+                                                           static_cast<double2*>(T), part, tick, running, 0);
+    c.count_launch();
+}
+
+template <int FAM>
+void launch_lik(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, int prec, const void* T, double* part,
+                unsigned* tick, unsigned* running) {
+    if (prec == 1)
+        k_lik<FAM, float2><<<tiles, FT, 0, c.stream>>>(st, segs, K, static_cast<const float2*>(T), part, tick,
+                                                       running);
+    else
+        k_lik<FAM, double2><<<tiles, FT, 0, c.stream>>>(st, segs, K, static_cast<const double2*>(T), part, tick,
+                                                        running);
+    c.count_launch();
+}
+
+template <int FAM>
+void launch_var(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, const FitIO& io, double* score,
+                double* A, double* part, unsigned* tick) {
+    k_var_terms<FAM><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.r2, io.u1, io.u2, io.pos, io.n_rows, score, A,
+                                                 part, tick);
+    c.count_launch();
+}
+
+std::vector<Seg> make_segs(const std::vector<uint64_t>& off, uint32_t& tiles) {
+    const size_t K = off.size() - 1;
+    std::vector<Seg> segs(K);
+    tiles = 0;
+    for (size_t m = 0; m < K; ++m) {
+        segs[m] = Seg{off[m], static_cast<uint32_t>(off[m + 1] - off[m]), tiles};
+        tiles += ftiles(off[m + 1] - off[m]);
+    }
+    return segs;
+}
+
+}  // namespace
+
+void init_tables() {
+    build_tables();
+    PCB_CUDA(cudaMemcpyToSymbol(c_frank_rho, h_frank_rho, sizeof h_frank_rho));
+    PCB_CUDA(cudaMemcpyToSymbol(c_frank_theta, h_frank_theta, sizeof h_frank_theta));
+    PCB_CUDA(cudaMemcpyToSymbol(c_gumbel_rho, h_gumbel_rho, sizeof h_gumbel_rho));
+    PCB_CUDA(cudaMemcpyToSymbol(c_gumbel_theta, h_gumbel_theta, sizeof h_gumbel_theta));
+}
+
+void run_fit(Ctx& c, const FitIO& io, void* d_out) {
+    const int K = static_cast<int>(io.off.size() - 1);
+    if (K <= 0) return;
+    cudaStream_t s = c.stream;
+    uint32_t tiles = 0;
+    std::vector<Seg> segs = make_segs(io.off, tiles);
+    auto* d_segs = c.ws.get_t<Seg>("fit.segs", K);
+    auto* st = c.ws.get_t<BlockState>("fit.state", K);
+    auto* part = c.ws.get_t<double>("fit.partials", static_cast<size_t>(tiles) * 4 + 4);
+    auto* tick = c.ws.get_t<unsigned>("fit.tickets", K);
+    auto* running = c.ws.get_t<unsigned>("fit.running", 1);
+    auto* h_running = static_cast<unsigned*>(c.host_staging(sizeof(unsigned)));
+    PCB_CUDA(cudaMemcpyAsync(d_segs, segs.data(), K * sizeof(Seg), cudaMemcpyHostToDevice, s));
+    PCB_CUDA(cudaMemsetAsync(tick, 0, K * sizeof(unsigned), s));
+    PCB_CUDA(cudaMemsetAsync(running, 0, sizeof(unsigned), s));
+    k_init_state<<<(K + 127) / 128, 128, 0, s>>>(st, d_segs, K, io.bad, running, io.theta_in);
+    c.count_launch();
+    const int fam = io.family;
+    if (tiles == 0) return;
+    cudaEvent_t* ev = c.ev;
+    PCB_CUDA(cudaEventRecord(ev[1], s));
+    if (io.do_fit) {
+        void* T = nullptr;
+        if (fam != kGaussian)
+            T = c.ws.get("fit.T", io.n_rows * (io.precision == 1 ? sizeof(float2) : sizeof(double2)));
+        if (fam == kGaussian) launch_prepare<kGaussian>(c, tiles, st, d_segs, K, io, T, part, tick, running);
+        else if (fam == kFrank) launch_prepare<kFrank>(c, tiles, st, d_segs, K, io, T, part, tick, running);
+        else launch_prepare<kGumbel>(c, tiles, st, d_segs, K, io, T, part, tick, running);
+        PCB_CUDA(cudaEventRecord(ev[2], s));
+        float lik_ms = 0.0f;
+        int lik_launches = 0;
+        if (fam != kGaussian) {
+            for (int pass = 0; pass < kMaxPasses; ++pass) {
+                PCB_CUDA(cudaEventRecord(ev[6], s));
+                if (fam == kFrank) launch_lik<kFrank>(c, tiles, st, d_segs, K, io.precision, T, part, tick, running);
+                else launch_lik<kGumbel>(c, tiles, st, d_segs, K, io.precision, T, part, tick, running);
+                PCB_CUDA(cudaEventRecord(ev[7], s));
+                PCB_CUDA(cudaMemcpyAsync(h_running, running, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+                PCB_CUDA(cudaStreamSynchronize(s));
+                float ms = 0.0f;
+                PCB_CUDA(cudaEventElapsedTime(&ms, ev[6], ev[7]));
+                lik_ms += ms;
+                ++lik_launches;
+                if (*h_running == 0) break;
+            }
+        }
+        PCB_CUDA(cudaEventRecord(ev[3], s));
+        c.stage_ms[5] = lik_ms;
+        c.stage_ms[6] = lik_launches;
+    } else {
+        PCB_CUDA(cudaEventRecord(ev[2], s));
+        PCB_CUDA(cudaEventRecord(ev[3], s));
+        c.stage_ms[5] = 0.0;
+        c.stage_ms[6] = 0;
+    }
+    if (io.do_variance) {
+        auto* score = c.ws.get_t<double>("fit.score", io.n_rows);
+        auto* A = c.ws.get_t<double>("fit.A", 2 * io.n_rows);
+        if (fam == kGaussian) launch_var<kGaussian>(c, tiles, st, d_segs, K, io, score, A, part, tick);
+        else if (fam == kFrank) launch_var<kFrank>(c, tiles, st, d_segs, K, io, score, A, part, tick);
+        else launch_var<kGumbel>(c, tiles, st, d_segs, K, io, score, A, part, tick);
+        k_suffix<<<2 * K, 1024, 0, s>>>(st, d_segs, K, io.n_rows, A);
+        k_var_final<<<tiles, FT, 0, s>>>(st, d_segs, K, io.lt, io.n_rows, score, A, part, tick);
+        c.count_launch(2);
+    }
+    PCB_CUDA(cudaEventRecord(ev[4], s));
+    k_finalize<<<(K + 127) / 128, 128, 0, s>>>(st, K, static_cast<RecordOut*>(d_out), io.do_variance ? 1 : 0);
+    c.count_launch();
+    PCB_CUDA(cudaEventRecord(ev[5], s));
+}
+
+void run_loglik(Ctx& c, int family, const double* d_theta, const double* u1, const double* u2,
+                const std::vector<uint64_t>& off, double* d_out) {
+    const int K = static_cast<int>(off.size() - 1);
+    uint32_t tiles = 0;
+    std::vector<Seg> segs = make_segs(off, tiles);
+    auto* d_segs = c.ws.get_t<Seg>("fit.segs", K);
+    auto* part = c.ws.get_t<double>("fit.partials", static_cast<size_t>(tiles) * 4 + 4);
+    auto* tick = c.ws.get_t<unsigned>("fit.tickets", K);
+    PCB_CUDA(cudaMemcpyAsync(d_segs, segs.data(), K * sizeof(Seg), cudaMemcpyHostToDevice, c.stream));
+    PCB_CUDA(cudaMemsetAsync(tick, 0, K * sizeof(unsigned), c.stream));
+    PCB_CUDA(cudaMemsetAsync(d_out, 0, K * sizeof(double), c.stream));
+    if (tiles == 0) return;
+    k_loglik<<<tiles, FT, 0, c.stream>>>(d_segs, K, d_theta, u1, u2, family, part, tick, d_out);
+    c.count_launch();
+}
+
+}  // namespace pcb

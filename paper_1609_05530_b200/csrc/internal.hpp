@@ -1,0 +1,145 @@
+// Host-side internals shared by the library's translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace pcb {
+
+// Errors carry a pcb_status code; the C-ABI layer converts them.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PCB_CUDA(call)                                                                                  \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            throw ::pcb::Error(5, std::string(#call) + " failed: " + cudaGetErrorString(e_) + " at " + \
+                                      __FILE__ + ":" + std::to_string(__LINE__));                       \
+    } while (0)
+
+// Growable cached device buffers, keyed by name.
+struct Workspace {
+    struct Buf {
+        void* p = nullptr;
+        size_t bytes = 0;
+    };
+    std::map<std::string, Buf> bufs;
+    void* get(const std::string& name, size_t bytes) {
+        Buf& b = bufs[name];
+        if (b.bytes < bytes) {
+            if (b.p) cudaFree(b.p);
+            b.p = nullptr;
+            b.bytes = 0;
+            const size_t want = bytes < 256 ? 256 : bytes;
+            PCB_CUDA(cudaMalloc(&b.p, want));
+            b.bytes = want;
+        }
+        return b.p;
+    }
+    template <class T>
+    T* get_t(const std::string& name, size_t count) {
+        return static_cast<T*>(get(name, count * sizeof(T)));
+    }
+    void release() {
+        for (auto& kv : bufs)
+            if (kv.second.p) cudaFree(kv.second.p);
+        bufs.clear();
+    }
+    ~Workspace() { release(); }
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    Workspace ws;
+    uint64_t launches = 0;
+    double stage_ms[8] = {0};
+    int n_stage = 0;
+    cudaEvent_t ev[8] = {};
+    // pinned host staging for small results
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    void* host_staging(size_t bytes) {
+        if (pinned_bytes < bytes) {
+            if (pinned) cudaFreeHost(pinned);
+            pinned = nullptr;
+            PCB_CUDA(cudaMallocHost(&pinned, bytes));
+            pinned_bytes = bytes;
+        }
+        return pinned;
+    }
+    void count_launch(int n = 1) {
+        launches += static_cast<uint64_t>(n);
+        PCB_CUDA(cudaGetLastError());
+    }
+};
+
+// ---------------------------------------------------------------- ranks
+// Segment-local bit-exact rank outputs, [2][n_rows] u32 each:
+//   r2  = (i+1)+(j+1), twice the 1-based average rank of the tie run i..j
+//   pos = unique stable sorted position (ties ordered by row index)
+//   lt  = i, the tie run's first sorted position
+struct RankOut {
+    uint32_t* r2;
+    uint32_t* pos;
+    uint32_t* lt;
+};
+
+// Ranks both columns of every segment. `bad` (n_seg int32, device) is set
+// non-zero for segments with non-finite values (validate_data).
+void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_rows, const std::vector<uint64_t>& off,
+               RankOut out, int32_t* d_bad);
+
+// u = (0.5*r2) * (1/(n_m+1)), bit-exact to normalized_rank_column
+void ranks_to_u(Ctx& c, const uint32_t* r2, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
+                double* u2);
+
+// ---------------------------------------------------------------- fit
+struct FitIO {
+    int family = 0;
+    int precision = 0;
+    uint64_t n_rows = 0;
+    std::vector<uint64_t> off;  // host offsets (n_seg + 1)
+    // exactly one source of (u, v): explicit arrays or rank pairs
+    const double* u1 = nullptr;
+    const double* u2 = nullptr;
+    const uint32_t* r2 = nullptr;  // [2][n_rows]
+    const uint32_t* pos = nullptr;
+    const uint32_t* lt = nullptr;
+    const int32_t* bad = nullptr;  // per segment, may be null
+    const double* theta_in = nullptr;  // device: skip the fit, evaluate at these (variance API)
+    bool do_fit = true;
+    bool do_variance = true;
+};
+
+// Runs prepare -> init -> Newton passes -> variance; writes n_seg
+// pcb_fit_result-compatible records (device) into d_out.
+void run_fit(Ctx& c, const FitIO& io, void* d_out_records);
+
+void run_loglik(Ctx& c, int family, const double* d_theta, const double* u1, const double* u2,
+                const std::vector<uint64_t>& off, double* d_out);
+
+void run_combine(Ctx& c, const void* d_records, uint64_t n, double* d_weights, double* d_out3);
+
+void run_sample(Ctx& c, int family, double theta, uint64_t n_total, uint64_t k_total, uint64_t first,
+                uint64_t last, uint64_t base_seed, double* d_col1, double* d_col2);
+
+void run_strided_gather(Ctx& c, const double* src, uint64_t n_rows, uint64_t m, double* dst);
+
+double run_fp64_peak(Ctx& c);
+
+void init_tables();
+
+}  // namespace pcb

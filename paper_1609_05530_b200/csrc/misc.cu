@@ -1,0 +1,219 @@
+// K6 combine, K7 sample, strided-partition gather, FP64 peak probe.
+#include <cmath>
+#include <vector>
+
+#include "devmath.cuh"
+#include "internal.hpp"
+
+namespace pcb {
+namespace {
+
+struct RecordIn {  // == pcb_fit_result
+    double theta_hat, sigma2, loglik;
+    uint64_t n;
+    int32_t iterations, converged, status, reserved;
+};
+
+// combine: w_m = 1/sigma2_m over converged blocks with a
+// finite positive variance; theta_c = sum w theta / sum w. One CTA, fixed
+// strided assignment + fixed tree => bitwise identical for any split of the
+// blocks across GPUs (the gathered record array is the same bytes).
+__global__ void __launch_bounds__(1024) k_combine(const RecordIn* r, uint64_t n, double* weights, double* out) {
+    double v[3] = {0.0, 0.0, 0.0};
+    for (uint64_t m = threadIdx.x; m < n; m += blockDim.x) {
+        const RecordIn x = r[m];
+        const bool ok = x.converged && x.sigma2 > 0.0 && isfinite(x.sigma2);
+        const double w = ok ? 1.0 / x.sigma2 : 0.0;
+        if (weights) weights[m] = w;
+        if (ok) {
+            v[0] += w;
+            v[1] += w * x.theta_hat;
+            v[2] += 1.0;
+        }
+    }
+    __shared__ double sh[32 * 3];
+    block_sum<3>(v, sh);
+    if (threadIdx.x == 0) {
+        out[0] = v[2] > 0.0 ? v[1] / v[0] : NAN;  // theta_combined
+        out[1] = v[0];                            // total weight
+        out[2] = v[2];                            // blocks used
+    }
+}
+
+// ------------------------------------------------------------------ sampler
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {  // rng.hpp:15-20
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ double unit_draw(uint64_t seed, uint64_t d) {  // rng.hpp:40-42
+    return (static_cast<double>(splitmix64(seed + d * 0x9e3779b97f4a7c15ull) >> 11) + 0.5) * 0x1p-53;
+}
+__device__ __forceinline__ double clamp_sample(double u) { return fmin(fmax(u, 1e-15), 1.0 - 1e-15); }
+
+// Counter-based per-block streams: point i of block m consumes draws
+// 4i..4i+3 of splitmix64(seed_m + d*gamma); transforms follow
+// copula.hpp:365-407 (Gaussian Box-Muller pair with the cached twin,
+// Frank conditional inversion, Gumbel Marshall-Olkin with a CMS stable).
+template <int FAM>
+__global__ void k_sample(double theta, uint64_t n_total, uint64_t k_total, uint64_t first, uint64_t row0,
+                         uint64_t rows, const uint64_t* seeds, double* c1, double* c2) {
+    const uint64_t q = n_total / k_total;
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < rows;
+         r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t g = row0 + r;  // global row
+        uint64_t m = g / q;
+        if (m >= k_total) m = k_total - 1;
+        const uint64_t i = g - m * q;
+        const uint64_t seed = seeds[m - first];
+        const double U0 = unit_draw(seed, 4 * i), U1 = unit_draw(seed, 4 * i + 1);
+        double a, b;
+        if (FAM == kGaussian) {
+            const double rr = sqrt(-2.0 * log(U0));
+            double sn, cs;
+            sincos(2.0 * 3.14159265358979323846 * U1, &sn, &cs);
+            const double z1 = rr * cs, z2 = rr * sn;
+            const double s = sqrt(1.0 - theta * theta);
+            a = clamp_sample(0.5 * erfc(-z1 * 0x1.6a09e667f3bcdp-1));
+            b = clamp_sample(0.5 * erfc(-(theta * z1 + s * z2) * 0x1.6a09e667f3bcdp-1));
+        } else if (FAM == kFrank) {
+            const double t = fabs(theta);
+            const double d = expm1(-t);
+            const double v = -log1p(U1 * d / (U1 + (1.0 - U1) * exp(-t * U0))) / t;
+            a = clamp_sample(U0);
+            b = clamp_sample(theta < 0.0 ? 1.0 - v : v);
+        } else {
+            if (theta == 1.0) {
+                a = U0;
+                b = U1;
+            } else {
+                const double al = 1.0 / theta;
+                const double th = 3.14159265358979323846 * U0;
+                const double w = -log(U1);
+                const double s1 = sin(al * th), s2 = sin((1.0 - al) * th), s = sin(th);
+                const double frail = pow(s2 / w, (1.0 - al) / al) * s1 / pow(s, 1.0 / al);
+                const double e1 = -log(unit_draw(seed, 4 * i + 2));
+                const double e2 = -log(unit_draw(seed, 4 * i + 3));
+                a = clamp_sample(exp(-pow(e1 / frail, al)));
+                b = clamp_sample(exp(-pow(e2 / frail, al)));
+            }
+        }
+        c1[r] = a;
+        c2[r] = b;
+    }
+}
+
+uint64_t h_splitmix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// strided partition: block m = rows i with i mod M == m
+__global__ void k_strided(const double* src, uint64_t n, uint64_t M, double* dst) {
+    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
+         j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        // destination j -> (block m, index k): block m has ceil((n-m)/M) rows
+        const uint64_t q = n / M, rem = n % M;  // blocks < rem have q+1 rows
+        uint64_t m, k;
+        if (j < rem * (q + 1)) {
+            m = j / (q + 1);
+            k = j - m * (q + 1);
+        } else {
+            const uint64_t jj = j - rem * (q + 1);
+            m = rem + jj / q;
+            k = jj - (m - rem) * q;
+        }
+        dst[j] = src[m + k * M];
+    }
+}
+
+__global__ void k_dfma(double* out, int iters) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+    double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double b = 0.999999999, c = 1e-12;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            a0 = fma(a0, b, c);
+            a1 = fma(a1, b, c);
+            a2 = fma(a2, b, c);
+            a3 = fma(a3, b, c);
+            a4 = fma(a4, b, c);
+            a5 = fma(a5, b, c);
+            a6 = fma(a6, b, c);
+            a7 = fma(a7, b, c);
+        }
+    }
+    const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+}  // namespace
+
+void run_combine(Ctx& c, const void* d_records, uint64_t n, double* d_weights, double* d_out3) {
+    k_combine<<<1, 1024, 0, c.stream>>>(static_cast<const RecordIn*>(d_records), n, d_weights, d_out3);
+    c.count_launch();
+}
+
+void run_sample(Ctx& c, int family, double theta, uint64_t n_total, uint64_t k_total, uint64_t first, uint64_t last,
+                uint64_t base_seed, double* d_col1, double* d_col2) {
+    const uint64_t q = n_total / k_total;
+    const uint64_t row0 = first * q;
+    const uint64_t row1 = last == k_total ? n_total : last * q;
+    const uint64_t rows = row1 - row0;
+    std::vector<uint64_t> seeds(last - first);
+    for (uint64_t m = first; m < last; ++m) {  // mix_seed(base, {family, n, K, m}), rng.hpp:24-29
+        uint64_t h = h_splitmix64(base_seed);
+        h = h_splitmix64(h ^ static_cast<uint64_t>(family));
+        h = h_splitmix64(h ^ n_total);
+        h = h_splitmix64(h ^ k_total);
+        h = h_splitmix64(h ^ m);
+        seeds[m - first] = h;
+    }
+    auto* d_seeds = c.ws.get_t<uint64_t>("sample.seeds", seeds.size());
+    PCB_CUDA(cudaMemcpyAsync(d_seeds, seeds.data(), seeds.size() * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                             c.stream));
+    const int threads = 256;
+    const uint64_t want = (rows + threads - 1) / threads;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(want, 148ull * 64));
+    if (rows == 0) return;
+    if (family == kGaussian)
+        k_sample<kGaussian><<<grid, threads, 0, c.stream>>>(theta, n_total, k_total, first, row0, rows, d_seeds, d_col1,
+                                                            d_col2);
+    else if (family == kFrank)
+        k_sample<kFrank><<<grid, threads, 0, c.stream>>>(theta, n_total, k_total, first, row0, rows, d_seeds, d_col1,
+                                                         d_col2);
+    else
+        k_sample<kGumbel><<<grid, threads, 0, c.stream>>>(theta, n_total, k_total, first, row0, rows, d_seeds, d_col1,
+                                                          d_col2);
+    c.count_launch();
+}
+
+void run_strided_gather(Ctx& c, const double* src, uint64_t n_rows, uint64_t m, double* dst) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n_rows + 255) / 256, 148ull * 64));
+    k_strided<<<grid, 256, 0, c.stream>>>(src, n_rows, m, dst);
+    c.count_launch();
+}
+
+double run_fp64_peak(Ctx& c) {
+    int sms = 0;
+    PCB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    auto* out = c.ws.get_t<double>("peak.out", 1024);
+    const int iters = 4096, threads = 512, blocks = sms * 4;
+    cudaEvent_t a = c.ev[6], b = c.ev[7];
+    k_dfma<<<blocks, threads, 0, c.stream>>>(out, 64);  // warm-up
+    PCB_CUDA(cudaEventRecord(a, c.stream));
+    k_dfma<<<blocks, threads, 0, c.stream>>>(out, iters);
+    PCB_CUDA(cudaEventRecord(b, c.stream));
+    PCB_CUDA(cudaEventSynchronize(b));
+    c.count_launch(2);
+    float ms = 0.0f;
+    PCB_CUDA(cudaEventElapsedTime(&ms, a, b));
+    const double instr = static_cast<double>(blocks) * threads * iters * 16.0 * 8.0;
+    return instr / (ms * 1e-3);
+}
+
+}  // namespace pcb

@@ -1,0 +1,479 @@
+// K1 seg_rank — bit-exact segment-local average ranks for sm_100a.
+//
+// Replaces detail::normalized_rank_column (pseudo_obs.hpp:44-65): for each
+// (segment, column) the reference index-sorts by (value, index) and gives a
+// tie run i..j the average rank 0.5*((i+1)+(j+1)). The GPU never sorts:
+// ranking only needs, per element, lt = #{values < x} and eq = #{values == x}
+// in its segment (plus the number of equal values with a smaller row index,
+// which yields a unique stable position for the variance scatter).
+//
+// Algorithm (one "level" = 6 launches over every range at once):
+//   minmax  per-range key / index extremes (64-bit order-preserving keys,
+//           -0.0 == +0.0), fused non-finite check (validate_data,
+//           pseudo_obs.hpp:30-37)
+//   resolve per-range bucket map: value-linear (level 0), key-linear, or
+//           row-index-linear for a range whose keys are all equal (a tie run)
+//   hist    bucket counts (monotone bucket map => buckets are ordered
+//           intervals of the sorted order; ties never straddle buckets)
+//   scan    per-range exclusive scan -> bucket starts; buckets above CAP are
+//           queued for the next level
+//   scatter (key, row) into the bucket's slots of a scratch array
+//   rank    per element: count smaller / equal / equal-with-smaller-row
+//           inside its (small) bucket; lt = range base + bucket start + #less
+// Oversize buckets become the next level's ranges (in place, ping-pong
+// scratch). Each level shrinks an oversize range's key span by >= nb, so
+// the refinement terminates in a few levels even for adversarial inputs;
+// uniform-marginal data (every BASELINE config) finishes in level 0.
+#include <algorithm>
+#include <cstring>
+
+#include "internal.hpp"
+
+namespace pcb {
+namespace {
+
+constexpr int RT = 256;
+constexpr uint32_t RTILE = 4096;
+constexpr uint32_t AVG = 8;    // target elements per bucket
+constexpr uint32_t CAP = 256;  // buckets larger than this are refined
+
+struct RankRange {
+    uint64_t src_base;  // level 0: row offset in the input column; else scratch position
+    uint64_t dst_base;  // scratch position of slot 0 of this range's buckets
+    uint64_t out_base;  // row offset of the segment (outputs at col*n_rows + out_base + row)
+    uint64_t bbase;     // first bucket slot
+    unsigned long long kmin, kmax;
+    uint64_t width;     // key-linear / index-linear bucket width
+    double scale, vmin_half;
+    uint32_t imin, imax;
+    uint32_t n, nb;
+    uint32_t lt_base, run_start, run_len;
+    uint32_t tile0;
+    int32_t mode;  // 0 value-linear, 1 key-linear, 2 tie run (index-linear)
+    int32_t col, seg, pad;
+};
+
+struct Oversize {
+    uint32_t range, start, count, pad;
+};
+
+__device__ __forceinline__ int range_of_tile(const RankRange* rr, int nr, uint32_t tile) {
+    int lo = 0, hi = nr - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rr[mid].tile0 <= tile) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <bool L0>
+__device__ __forceinline__ void load_elem(const RankRange& R, uint32_t i, const double* c0, const double* c1,
+                                          const unsigned long long* skey, const uint32_t* sidx,
+                                          unsigned long long& key, uint32_t& idx, bool& finite) {
+    if (L0) {
+        const double x = __ldg((R.col ? c1 : c0) + R.src_base + i);
+        finite = isfinite(x);
+        key = order_key(x);
+        idx = i;
+    } else {
+        key = skey[R.src_base + i];
+        idx = sidx[R.src_base + i];
+        finite = true;
+    }
+}
+
+__device__ __forceinline__ uint32_t bucket_of(const RankRange& R, unsigned long long key, uint32_t idx) {
+    if (R.mode == 0) {
+        const double v = key_value(key);
+        const double t = (0.5 * v - R.vmin_half) * R.scale;
+        return t < static_cast<double>(R.nb) ? static_cast<uint32_t>(t) : R.nb - 1;
+    }
+    if (R.mode == 1) return static_cast<uint32_t>((key - R.kmin) / R.width);
+    return static_cast<uint32_t>((idx - R.imin) / R.width);
+}
+
+template <bool L0>
+__global__ void __launch_bounds__(RT) k_minmax(RankRange* rr, int nr, const double* c0, const double* c1,
+                                              const unsigned long long* skey, const uint32_t* sidx, int32_t* bad) {
+    const int r = range_of_tile(rr, nr, blockIdx.x);
+    const RankRange R = rr[r];
+    const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
+    const uint32_t end = min(begin + RTILE, R.n);
+    unsigned long long kmn = ~0ull, kmx = 0ull;
+    uint32_t imn = ~0u, imx = 0u;
+    bool allfin = true;
+    for (uint32_t i = begin + threadIdx.x; i < end; i += RT) {
+        unsigned long long k;
+        uint32_t id;
+        bool fin;
+        load_elem<L0>(R, i, c0, c1, skey, sidx, k, id, fin);
+        allfin &= fin;
+        kmn = min(kmn, k);
+        kmx = max(kmx, k);
+        imn = min(imn, id);
+        imx = max(imx, id);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+        kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+        imn = min(imn, __shfl_xor_sync(0xffffffffu, imn, o));
+        imx = max(imx, __shfl_xor_sync(0xffffffffu, imx, o));
+    }
+    allfin = __all_sync(0xffffffffu, allfin);
+    __shared__ unsigned long long s_kmn[RT / 32], s_kmx[RT / 32];
+    __shared__ uint32_t s_imn[RT / 32], s_imx[RT / 32];
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_kmn[w] = kmn;
+        s_kmx[w] = kmx;
+        s_imn[w] = imn;
+        s_imx[w] = imx;
+        if (!allfin) s_bad = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < RT / 32; ++k) {
+            kmn = min(kmn, s_kmn[k]);
+            kmx = max(kmx, s_kmx[k]);
+            imn = min(imn, s_imn[k]);
+            imx = max(imx, s_imx[k]);
+        }
+        atomicMin(&rr[r].kmin, kmn);
+        atomicMax(&rr[r].kmax, kmx);
+        if (!L0) {
+            atomicMin(&rr[r].imin, imn);
+            atomicMax(&rr[r].imax, imx);
+        }
+        if (L0 && s_bad) bad[R.seg] = 1;
+    }
+}
+
+__global__ void k_resolve(RankRange* rr, int nr, int level0) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nr) return;
+    RankRange R = rr[r];
+    if (level0) {
+        R.imin = 0;
+        R.imax = R.n ? R.n - 1 : 0;
+    }
+    if (R.mode == 0) {
+        if (R.kmin == R.kmax) {
+            R.mode = 2;
+            R.run_start = R.lt_base;
+            R.run_len = R.n;
+        } else {
+            const double vmin = key_value(R.kmin), vmax = key_value(R.kmax);
+            const double hm = 0.5 * vmin;
+            const double d = 0.5 * vmax - hm;
+            const double sc = static_cast<double>(R.nb) / d;
+            if (isfinite(sc) && sc > 0.0 && isfinite(hm)) {
+                R.scale = sc;
+                R.vmin_half = hm;
+            } else {
+                R.mode = 1;
+            }
+        }
+    }
+    if (R.mode == 1) {
+        if (R.kmin == R.kmax) {
+            R.mode = 2;
+            R.run_start = R.lt_base;
+            R.run_len = R.n;
+        } else {
+            R.width = (R.kmax - R.kmin) / R.nb + 1;
+        }
+    }
+    if (R.mode == 2) R.width = static_cast<uint64_t>(R.imax - R.imin) / R.nb + 1;
+    rr[r] = R;
+}
+
+template <bool L0>
+__global__ void __launch_bounds__(RT) k_hist(const RankRange* rr, int nr, const double* c0, const double* c1,
+                                            const unsigned long long* skey, const uint32_t* sidx, uint32_t* hist) {
+    const int r = range_of_tile(rr, nr, blockIdx.x);
+    const RankRange R = rr[r];
+    const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
+    const uint32_t end = min(begin + RTILE, R.n);
+    for (uint32_t i = begin + threadIdx.x; i < end; i += RT) {
+        unsigned long long k;
+        uint32_t id;
+        bool fin;
+        load_elem<L0>(R, i, c0, c1, skey, sidx, k, id, fin);
+        atomicAdd(hist + R.bbase + bucket_of(R, k, id), 1u);
+    }
+}
+
+// One block per range: exclusive scan of the range's bucket counts.
+__global__ void __launch_bounds__(1024) k_scan(const RankRange* rr, const uint32_t* hist, uint32_t* bstart,
+                                              uint32_t* cursor, Oversize* ov, uint32_t* ov_count,
+                                              uint32_t ov_cap) {
+    const RankRange R = rr[blockIdx.x];
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint32_t base = 0; base < R.nb; base += blockDim.x) {
+        const uint32_t b = base + threadIdx.x;
+        const uint32_t c = b < R.nb ? hist[R.bbase + b] : 0u;
+        uint32_t x = c;  // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            uint32_t z = lane < static_cast<int>(blockDim.x >> 5) ? s_warp[lane] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+                if (lane >= o) z += y;
+            }
+            s_warp[lane] = z;
+        }
+        __syncthreads();
+        const uint32_t excl = s_carry + (w ? s_warp[w - 1] : 0u) + x - c;
+        if (b < R.nb) {
+            bstart[R.bbase + b] = excl;
+            cursor[R.bbase + b] = excl;
+            if (c > CAP) {
+                const uint32_t slot = atomicAdd(ov_count, 1u);
+                if (slot < ov_cap) ov[slot] = Oversize{blockIdx.x, excl, c, 0u};
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = excl + c;
+        __syncthreads();
+    }
+}
+
+template <bool L0>
+__global__ void __launch_bounds__(RT) k_scatter(const RankRange* rr, int nr, const double* c0, const double* c1,
+                                               const unsigned long long* skey, const uint32_t* sidx,
+                                               uint32_t* cursor, unsigned long long* dkey, uint32_t* didx) {
+    const int r = range_of_tile(rr, nr, blockIdx.x);
+    const RankRange R = rr[r];
+    const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
+    const uint32_t end = min(begin + RTILE, R.n);
+    for (uint32_t i = begin + threadIdx.x; i < end; i += RT) {
+        unsigned long long k;
+        uint32_t id;
+        bool fin;
+        load_elem<L0>(R, i, c0, c1, skey, sidx, k, id, fin);
+        const uint32_t slot = atomicAdd(cursor + R.bbase + bucket_of(R, k, id), 1u);
+        dkey[R.dst_base + slot] = k;
+        didx[R.dst_base + slot] = id;
+    }
+}
+
+// One thread per element of the scattered range; buckets <= CAP are ranked
+// by counting inside the bucket (L1-resident neighbours).
+__global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const unsigned long long* dkey,
+                                            const uint32_t* didx, const uint32_t* hist, const uint32_t* bstart,
+                                            uint64_t n_rows, uint32_t* o_r2, uint32_t* o_pos, uint32_t* o_lt) {
+    const int r = range_of_tile(rr, nr, blockIdx.x);
+    const RankRange R = rr[r];
+    const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
+    const uint32_t end = min(begin + RTILE, R.n);
+    for (uint32_t p = begin + threadIdx.x; p < end; p += RT) {
+        const unsigned long long k = dkey[R.dst_base + p];
+        const uint32_t id = didx[R.dst_base + p];
+        const uint32_t b = bucket_of(R, k, id);
+        const uint32_t cnt = hist[R.bbase + b];
+        if (cnt > CAP) continue;  // refined at the next level
+        const uint32_t s = bstart[R.bbase + b];
+        const unsigned long long* bk = dkey + R.dst_base + s;
+        const uint32_t* bi = didx + R.dst_base + s;
+        uint32_t lt, eq, pos;
+        if (R.mode == 2) {
+            uint32_t before = 0;
+            for (uint32_t q = 0; q < cnt; ++q) before += bi[q] < id;
+            lt = R.run_start;
+            eq = R.run_len;
+            pos = R.lt_base + s + before;
+        } else {
+            uint32_t less = 0, same = 0, before = 0;
+            for (uint32_t q = 0; q < cnt; ++q) {
+                const unsigned long long kq = bk[q];
+                less += kq < k;
+                const bool e = kq == k;
+                same += e;
+                before += e && (bi[q] < id);
+            }
+            lt = R.lt_base + s + less;
+            eq = same;
+            pos = lt + before;
+        }
+        const uint64_t o = static_cast<uint64_t>(R.col) * n_rows + R.out_base + id;
+        o_r2[o] = 2u * lt + eq + 1u;
+        o_pos[o] = pos;
+        o_lt[o] = lt;
+    }
+}
+
+__global__ void k_ranks_to_u(const Seg* segs, int nseg, const uint32_t* r2, uint64_t n_rows, double* u1, double* u2) {
+    const int m = seg_of_tile(segs, nseg, blockIdx.x);
+    const Seg S = segs[m];
+    const uint32_t begin = (blockIdx.x - S.tile0) * RTILE;
+    const uint32_t end = min(begin + RTILE, S.n);
+    const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);  // pseudo_obs.hpp:53
+    for (uint32_t i = begin + threadIdx.x; i < end; i += RT) {
+        const uint64_t row = S.begin + i;
+        // pseudo_obs.hpp:59-60: avg = 0.5*((i+1)+(j+1)); u = avg*scale
+        u1[row] = __dmul_rn(0.5 * static_cast<double>(r2[row]), scale);
+        u2[row] = __dmul_rn(0.5 * static_cast<double>(r2[n_rows + row]), scale);
+    }
+}
+
+uint32_t tiles_of(uint64_t n) { return static_cast<uint32_t>((n + RTILE - 1) / RTILE); }
+
+}  // namespace
+
+void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_rows, const std::vector<uint64_t>& off,
+               RankOut out, int32_t* d_bad) {
+    const size_t K = off.size() - 1;
+    if (K == 0 || n_rows == 0) return;
+    for (size_t m = 0; m < K; ++m)
+        if (off[m + 1] - off[m] >= (1ull << 30)) throw Error(2, "segment too large for 32-bit ranks");
+    cudaStream_t st = c.stream;
+    // ---- level 0: one range per (column, segment)
+    std::vector<RankRange> ranges;
+    ranges.reserve(2 * K);
+    uint64_t bsum = 0;
+    uint32_t tiles = 0;
+    for (int col = 0; col < 2; ++col)
+        for (size_t m = 0; m < K; ++m) {
+            RankRange R;
+            std::memset(&R, 0, sizeof R);
+            const uint64_t n = off[m + 1] - off[m];
+            R.src_base = off[m];
+            R.dst_base = static_cast<uint64_t>(col) * n_rows + off[m];
+            R.out_base = off[m];
+            R.n = static_cast<uint32_t>(n);
+            R.nb = std::max<uint32_t>(1u, static_cast<uint32_t>(n / AVG));
+            R.bbase = bsum;
+            R.kmin = ~0ull;
+            R.kmax = 0ull;
+            R.imin = ~0u;
+            R.imax = 0u;
+            R.mode = 0;
+            R.col = col;
+            R.seg = static_cast<int32_t>(m);
+            R.tile0 = tiles;
+            bsum += R.nb;
+            tiles += tiles_of(n);
+            ranges.push_back(R);
+        }
+    const uint64_t total = 2 * n_rows;
+    auto* keyA = c.ws.get_t<unsigned long long>("rank.keyA", total);
+    auto* idxA = c.ws.get_t<uint32_t>("rank.idxA", total);
+    const uint32_t ov_cap = static_cast<uint32_t>(total / CAP + 16);
+    auto* ov = c.ws.get_t<Oversize>("rank.ov", ov_cap);
+    auto* ovn = c.ws.get_t<uint32_t>("rank.ovn", 1);
+    int nr = static_cast<int>(ranges.size());
+    auto* d_rr = c.ws.get_t<RankRange>("rank.ranges", ranges.size());
+    auto* hist = c.ws.get_t<uint32_t>("rank.hist", bsum);
+    auto* bstart = c.ws.get_t<uint32_t>("rank.bstart", bsum);
+    auto* cursor = c.ws.get_t<uint32_t>("rank.cursor", bsum);
+    auto* h_ovn = static_cast<uint32_t*>(c.host_staging(sizeof(uint32_t)));
+
+    auto run_level = [&](bool l0, const unsigned long long* skey, const uint32_t* sidx, unsigned long long* dkey,
+                         uint32_t* didx, uint64_t nbuckets, uint32_t ntiles) {
+        PCB_CUDA(cudaMemcpyAsync(d_rr, ranges.data(), ranges.size() * sizeof(RankRange), cudaMemcpyHostToDevice, st));
+        PCB_CUDA(cudaMemsetAsync(hist, 0, nbuckets * sizeof(uint32_t), st));
+        PCB_CUDA(cudaMemsetAsync(ovn, 0, sizeof(uint32_t), st));
+        if (l0) k_minmax<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, d_bad);
+        else k_minmax<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, d_bad);
+        k_resolve<<<(nr + 127) / 128, 128, 0, st>>>(d_rr, nr, l0 ? 1 : 0);
+        if (l0) k_hist<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, hist);
+        else k_hist<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, hist);
+        k_scan<<<nr, 1024, 0, st>>>(d_rr, hist, bstart, cursor, ov, ovn, ov_cap);
+        if (l0) k_scatter<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
+        else k_scatter<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
+        k_rank<<<ntiles, RT, 0, st>>>(d_rr, nr, dkey, didx, hist, bstart, n_rows, out.r2, out.pos, out.lt);
+        c.count_launch(6);
+        PCB_CUDA(cudaMemcpyAsync(h_ovn, ovn, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        PCB_CUDA(cudaStreamSynchronize(st));
+        return *h_ovn;
+    };
+
+    uint32_t n_ov = run_level(true, nullptr, nullptr, keyA, idxA, bsum, tiles);
+    // ---- refinement levels (adversarial / heavily skewed inputs only)
+    unsigned long long *cur_key = keyA, *nxt_key = nullptr;
+    uint32_t *cur_idx = idxA, *nxt_idx = nullptr;
+    int level = 0;
+    while (n_ov > 0) {
+        if (++level > 80) throw Error(5, "rank refinement did not terminate");
+        if (n_ov > ov_cap) throw Error(5, "rank oversize list overflow");
+        std::vector<Oversize> hov(n_ov);
+        std::vector<RankRange> parents(ranges.size());
+        PCB_CUDA(cudaMemcpyAsync(hov.data(), ov, n_ov * sizeof(Oversize), cudaMemcpyDeviceToHost, st));
+        PCB_CUDA(cudaMemcpyAsync(parents.data(), d_rr, parents.size() * sizeof(RankRange), cudaMemcpyDeviceToHost, st));
+        PCB_CUDA(cudaStreamSynchronize(st));
+        if (!nxt_key) {
+            nxt_key = c.ws.get_t<unsigned long long>("rank.keyB", total);
+            nxt_idx = c.ws.get_t<uint32_t>("rank.idxB", total);
+        }
+        ranges.clear();
+        bsum = 0;
+        tiles = 0;
+        for (const Oversize& o : hov) {
+            const RankRange& P = parents[o.range];
+            RankRange R;
+            std::memset(&R, 0, sizeof R);
+            R.src_base = P.dst_base + o.start;
+            R.dst_base = R.src_base;
+            R.out_base = P.out_base;
+            R.n = o.count;
+            R.nb = std::max<uint32_t>(2u, o.count / AVG);
+            R.bbase = bsum;
+            R.kmin = ~0ull;
+            R.kmax = 0ull;
+            R.imin = ~0u;
+            R.imax = 0u;
+            R.lt_base = P.lt_base + o.start;
+            R.mode = P.mode == 2 ? 2 : 1;
+            R.run_start = P.run_start;
+            R.run_len = P.run_len;
+            R.col = P.col;
+            R.seg = P.seg;
+            R.tile0 = tiles;
+            bsum += R.nb;
+            tiles += tiles_of(o.count);
+            ranges.push_back(R);
+        }
+        nr = static_cast<int>(ranges.size());
+        d_rr = c.ws.get_t<RankRange>("rank.ranges", ranges.size());
+        hist = c.ws.get_t<uint32_t>("rank.hist", bsum);
+        bstart = c.ws.get_t<uint32_t>("rank.bstart", bsum);
+        cursor = c.ws.get_t<uint32_t>("rank.cursor", bsum);
+        n_ov = run_level(false, cur_key, cur_idx, nxt_key, nxt_idx, bsum, tiles);
+        std::swap(cur_key, nxt_key);
+        std::swap(cur_idx, nxt_idx);
+    }
+}
+
+void ranks_to_u(Ctx& c, const uint32_t* r2, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
+                double* u2) {
+    const size_t K = off.size() - 1;
+    std::vector<Seg> segs(K);
+    uint32_t tiles = 0;
+    for (size_t m = 0; m < K; ++m) {
+        segs[m] = Seg{off[m], static_cast<uint32_t>(off[m + 1] - off[m]), tiles};
+        tiles += tiles_of(off[m + 1] - off[m]);
+    }
+    if (tiles == 0) return;
+    auto* d_segs = c.ws.get_t<Seg>("u.segs", K);
+    PCB_CUDA(cudaMemcpyAsync(d_segs, segs.data(), K * sizeof(Seg), cudaMemcpyHostToDevice, c.stream));
+    k_ranks_to_u<<<tiles, RT, 0, c.stream>>>(d_segs, static_cast<int>(K), r2, n_rows, u1, u2);
+    c.count_launch();
+}
+
+}  // namespace pcb

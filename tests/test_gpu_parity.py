@@ -1,0 +1,264 @@
+"""Device-vs-oracle parity through the C-ABI (libparcop_b200.so) on a B200.
+
+Bars (BASELINE.json north_star): ranks bit-identical; theta-hat, sigma2,
+loglik and theta_combined within 1e-9 relative (fp64 path) or 1e-5 (fp32
+likelihood path) of the CPU oracle on the same bytes.
+"""
+import numpy as np
+import pytest
+
+import paper_1609_05530_b200 as pcb
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-9
+TOL32 = 1e-5
+FAMS = [(0, 0.5), (1, 5.0), (2, 2.0)]
+SWEEP = [(0, 0.2), (0, 0.8), (0, -0.5), (1, 2.0), (1, 10.0), (1, -4.0), (2, 1.5), (2, 3.0)]
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def oracle_ranks(orc, col, off):
+    return np.concatenate([orc.rank_column(col[int(off[m]):int(off[m + 1])]) for m in range(len(off) - 1)])
+
+
+def check_records(got, want, tol):
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert bool(g.converged) == bool(w.converged), (g, w.converged)
+        if not w.converged:
+            continue
+        assert rel(g.theta_hat, w.theta_hat) <= tol, (g.theta_hat, w.theta_hat)
+        assert rel(g.sigma2, w.sigma2) <= max(tol, 1e-9), (g.sigma2, w.sigma2)
+        if tol <= 1e-9:
+            assert rel(g.loglik, w.loglik) <= 1e-9 or abs(g.loglik - w.loglik) < 1e-9, (g.loglik, w.loglik)
+
+
+# ----------------------------------------------------------------- ranks
+@pytest.mark.parametrize("n,k", [(10000, 10), (100000, 10), (30000, 7), (2, 1), (4097, 1)])
+def test_ranks_bit_exact_random(ctx, orc, n, k):
+    rng = np.random.default_rng(n + k)
+    c1 = rng.standard_normal(n)
+    c2 = rng.exponential(size=n) * 1e3
+    off = np.linspace(0, n, k + 1).astype(np.uint64)
+    U = pcb.normalized_ranks(pcb.DataMatrix(c1, c2), off, ctx=ctx)
+    assert np.array_equal(U.u1, oracle_ranks(orc, c1, off))
+    assert np.array_equal(U.u2, oracle_ranks(orc, c2, off))
+
+
+def test_ranks_match_compiled_reference(ctx, ref):
+    rng = np.random.default_rng(7)
+    c1 = np.round(rng.standard_normal(5000), 2)  # many ties
+    c2 = rng.uniform(size=5000)
+    U = pcb.normalized_ranks(pcb.DataMatrix(c1, c2), ctx=ctx)
+    r1, r2 = ref.normalized_ranks(c1, c2)
+    assert np.array_equal(U.u1, r1) and np.array_equal(U.u2, r2)
+
+
+ADVERSARIAL = {
+    "spec_example": ([3.1, 1.2, 7.5], [1.0, 1.0, 2.0]),
+    "signed_zero": ([0.0, -0.0, 1.0, -1.0], [-0.0, 0.0, -0.0, 0.0]),
+    "constant": (np.full(5000, 3.0), np.full(5000, -2.0)),
+    "few_values": (np.arange(20000) % 7 * 1.0, np.arange(20000) % 3 * 1.0),
+    "big_tie_runs": (np.repeat([1.0, 2.0, 3.0], 3000), np.tile([5.0, 4.0], 4500)),
+    "geometric": (2.0 ** np.arange(-500, 500, 1.0), -(2.0 ** np.arange(-500, 500, 1.0))),
+    "huge_range": (np.array([-1e308, 1e308, 0.0, 5e-324, -5e-324, 1.0] * 50), np.linspace(-1, 1, 300)),
+    "one_outlier": (np.r_[np.zeros(9999) + 0.5, 1e300], np.r_[np.linspace(0, 1, 5000), np.full(5000, 0.25)]),
+    "clustered": (np.r_[np.random.default_rng(3).uniform(0, 1e-9, 8000), np.random.default_rng(4).uniform(5, 6, 8)],
+                  np.random.default_rng(5).standard_cauchy(8008)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(ADVERSARIAL))
+def test_ranks_adversarial(ctx, orc, name):
+    c1, c2 = (np.asarray(a, np.float64) for a in ADVERSARIAL[name])
+    U = pcb.normalized_ranks(pcb.DataMatrix(c1, c2), ctx=ctx)
+    w1, w2 = orc.normalized_ranks(c1, c2)
+    assert np.array_equal(U.u1, w1), name
+    assert np.array_equal(U.u2, w2), name
+
+
+def test_ranks_ragged_segments(ctx, orc):
+    rng = np.random.default_rng(11)
+    sizes = [2, 3, 31, 4096, 4097, 8191, 100, 17000, 2]
+    off = np.r_[0, np.cumsum(sizes)].astype(np.uint64)
+    n = int(off[-1])
+    c1 = np.round(rng.standard_normal(n), 1)
+    c2 = rng.uniform(size=n)
+    U = pcb.normalized_ranks(pcb.DataMatrix(c1, c2), off, ctx=ctx)
+    assert np.array_equal(U.u1, oracle_ranks(orc, c1, off))
+    assert np.array_equal(U.u2, oracle_ranks(orc, c2, off))
+
+
+def test_ranks_nonfinite_raises(ctx):
+    with pytest.raises(pcb.DomainError):
+        pcb.normalized_ranks(pcb.DataMatrix([1.0, np.nan, 2.0], [1.0, 2.0, 3.0]), ctx=ctx)
+    with pytest.raises(pcb.DomainError):
+        pcb.normalized_ranks(pcb.DataMatrix([1.0, 2.0, 3.0], [np.inf, 2.0, 3.0]), ctx=ctx)
+    with pytest.raises(ValueError):
+        pcb.normalized_ranks(pcb.DataMatrix([1.0], [1.0]), ctx=ctx)
+
+
+# ------------------------------------------------------------- fit path
+@pytest.mark.parametrize("fam,theta", FAMS + SWEEP)
+def test_fit_blocks_parity(ctx, orc, fam, theta):
+    n, k = 40000, 8
+    X = pcb.sample_matrix(fam, theta, n, k, ctx=ctx)
+    off = orc.partition(n, k)
+    got = pcb.fit_blocks(fam, X, off, ctx=ctx)
+    want = orc.fit_blocks(fam, X.col1, X.col2, off)
+    check_records(got, want, TOL64)
+    res = pcb.fit_parallel(fam, X, k, ctx=ctx)
+    tc, w, used = orc.combine(want)
+    assert res.blocks_used == used
+    assert rel(res.theta_combined, tc) <= TOL64
+    assert np.allclose(res.weights, w, rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("fam,theta", FAMS + [(1, -4.0), (2, 3.0)])
+def test_fit_fp32_parity(ctx, orc, fam, theta):
+    n, k = 40000, 4
+    X = pcb.sample_matrix(fam, theta, n, k, ctx=ctx)
+    off = orc.partition(n, k)
+    got = pcb.fit_blocks(fam, X, off, precision=pcb.Precision.fp32, ctx=ctx)
+    want = orc.fit_blocks(fam, X.col1, X.col2, off)
+    check_records(got, want, TOL32)
+
+
+@pytest.mark.parametrize("fam,theta", FAMS)
+def test_fit_from_pseudo_sample(ctx, orc, fam, theta):
+    n = 5000
+    X = pcb.sample_matrix(fam, theta, n, 1, ctx=ctx)
+    u1, u2 = orc.normalized_ranks(X.col1, X.col2)
+    g = pcb.fit(fam, pcb.PseudoSample(u1, u2), ctx=ctx)
+    w = orc.fit(fam, u1, u2)
+    check_records([g], [w], TOL64)
+    s2 = pcb.asymptotic_variance(fam, w.theta_hat, pcb.PseudoSample(u1, u2), ctx=ctx)
+    assert rel(s2, orc.asymptotic_variance(fam, w.theta_hat, u1, u2)) <= TOL64
+    ll = pcb.pseudo_loglik(fam, w.theta_hat, pcb.PseudoSample(u1, u2), ctx=ctx)
+    assert rel(ll, orc.pseudo_loglik(fam, w.theta_hat, u1, u2)) <= 1e-11
+
+
+def test_fit_with_ties_uses_tie_run_suffix(ctx, orc):
+    rng = np.random.default_rng(21)
+    n = 6000
+    z = rng.standard_normal(n)
+    c1 = np.round(z, 1)
+    c2 = np.round(0.6 * z + 0.8 * rng.standard_normal(n), 1)
+    u1, u2 = orc.normalized_ranks(c1, c2)
+    for fam in (0, 1, 2):
+        g = pcb.fit(fam, pcb.PseudoSample(u1, u2), ctx=ctx)
+        w = orc.fit(fam, u1, u2)
+        check_records([g], [w], TOL64)
+        naive = orc.asymptotic_variance(fam, w.theta_hat, u1, u2, naive=True)
+        assert rel(g.sigma2, naive) <= 1e-9
+
+
+def test_pseudo_loglik_segments(ctx, orc):
+    X = pcb.sample_matrix(1, 5.0, 9000, 3, ctx=ctx)
+    off = orc.partition(9000, 3)
+    U = pcb.normalized_ranks(X, off, ctx=ctx)
+    th = np.array([4.0, 5.0, -2.0])
+    got = pcb.pseudo_loglik(1, th, U, segments=off, ctx=ctx)
+    for m in range(3):
+        a, b = int(off[m]), int(off[m + 1])
+        assert rel(got[m], orc.pseudo_loglik(1, th[m], U.u1[a:b], U.u2[a:b])) <= 1e-11
+
+
+def test_domain_errors(ctx):
+    U = pcb.PseudoSample(np.array([0.2, 0.5, 0.7]), np.array([0.3, 0.6, 0.1]))
+    with pytest.raises(pcb.DomainError):
+        pcb.pseudo_loglik(0, 1.0, U, ctx=ctx)
+    with pytest.raises(pcb.DomainError):
+        pcb.pseudo_loglik(2, 0.9, U, ctx=ctx)
+    with pytest.raises(pcb.DomainError):
+        pcb.pseudo_loglik(1, 0.0, U, ctx=ctx)
+    with pytest.raises(pcb.DomainError):
+        pcb.fit(0, pcb.PseudoSample(np.array([0.2, 1.0] * 20), np.array([0.3, 0.5] * 20)), ctx=ctx)
+
+
+def test_small_block_not_converged_not_error(ctx):
+    X = pcb.sample_matrix(0, 0.5, 100, 1, ctx=ctx)
+    g = pcb.fit_blocks(0, X, [0, 20, 100], ctx=ctx)
+    assert not g[0].converged and g[0].status == 4
+    assert g[1].converged
+
+
+# ---------------------------------------------------- determinism / G split
+def test_bitwise_determinism_and_gpu_split(ctx):
+    n, k = 200000, 16
+    fam = 2
+    X = pcb.sample_matrix(fam, 2.0, n, k, ctx=ctx)
+    off = pcb.partition(n, k).offsets
+    a = pcb.fit_blocks(fam, X, off, ctx=ctx)
+    b = pcb.fit_blocks(fam, X, off, ctx=ctx)
+    assert [r.theta_hat for r in a] == [r.theta_hat for r in b]
+    assert [r.sigma2 for r in a] == [r.sigma2 for r in b]
+    # the same blocks fitted as two "GPU shards" (contiguous block ranges), then combined
+    h = int(off[k // 2])
+    s0 = pcb.fit_blocks(fam, pcb.DataMatrix(X.col1[:h], X.col2[:h]), off[:k // 2 + 1], ctx=ctx)
+    s1 = pcb.fit_blocks(fam, pcb.DataMatrix(X.col1[h:], X.col2[h:]), off[k // 2:] - off[k // 2], ctx=ctx)
+    assert [r.theta_hat for r in s0 + s1] == [r.theta_hat for r in a]
+    assert pcb.combine(s0 + s1, ctx=ctx).theta_combined == pcb.combine(a, ctx=ctx).theta_combined
+
+
+def test_sampler_shards_identical(ctx):
+    full = pcb.sample_matrix(1, 5.0, 10000, 10, ctx=ctx)
+    part = pcb.sample_matrix(1, 5.0, 10000, 10, first_block=3, last_block=7, ctx=ctx)
+    assert np.array_equal(full.col1[3000:7000], part.col1)
+    assert np.array_equal(full.col2[3000:7000], part.col2)
+
+
+def test_sampler_integer_stream_matches_oracle(ctx, orc):
+    # Frank u = the raw uniform draw: bit-identical to the oracle's counter-based stream
+    n, k = 4000, 4
+    X = pcb.sample_matrix(1, 5.0, n, k, ctx=ctx)
+    off = orc.partition(n, k)
+    c1, c2 = orc.sample_blocks(1, 5.0, n, k, off, 0, k)
+    assert np.array_equal(X.col1, np.clip(c1, 1e-15, 1 - 1e-15))
+    assert np.allclose(X.col2, c2, rtol=1e-13, atol=0)
+    for fam, th in ((0, 0.5), (2, 2.0)):
+        X = pcb.sample_matrix(fam, th, n, k, ctx=ctx)
+        c1, c2 = orc.sample_blocks(fam, th, n, k, off, 0, k)
+        assert np.allclose(X.col1, c1, rtol=1e-12, atol=1e-300)
+
+
+def test_strided_scheme(ctx, orc):
+    n, k = 10007, 5
+    X = pcb.sample_matrix(0, 0.5, n, 1, ctx=ctx)
+    res = pcb.fit_parallel(0, X, k, scheme=pcb.Scheme.Strided, ctx=ctx)
+    p = pcb.partition(n, k, pcb.Scheme.Strided)
+    recs = []
+    for m in range(k):
+        rows = np.arange(m, n, k)
+        assert len(rows) == int(p.offsets[m + 1] - p.offsets[m])
+        recs.append(orc.fit_blocks(0, X.col1[rows], X.col2[rows], [0, len(rows)])[0])
+    check_records(res.per_block, recs, TOL64)
+
+
+def test_m1_equals_full_fit(ctx):
+    X = pcb.sample_matrix(2, 2.0, 20000, 1, ctx=ctx)
+    res = pcb.fit_parallel(2, X, 1, ctx=ctx)
+    full = pcb.fit(2, pcb.normalized_ranks(X, ctx=ctx), ctx=ctx)
+    assert res.theta_combined == full.theta_hat
+
+
+def test_c1_golden_fixture(ctx):
+    """configs[0] on the reference's own sampler bytes (tests/golden)."""
+    import json
+    import os
+    d = os.path.join(os.path.dirname(__file__), "golden")
+    data = np.load(os.path.join(d, "c1_gaussian_rho05_n1e4.npz"))
+    meta = json.load(open(os.path.join(d, "c1_expected.json")))
+    X = pcb.DataMatrix(data["col1"], data["col2"])
+    res = pcb.fit_parallel(0, X, 10, ctx=ctx)
+    for g, w in zip(res.per_block, meta["per_block"]):
+        assert rel(g.theta_hat, w["theta_hat"]) <= TOL64
+        assert rel(g.sigma2, w["sigma2"]) <= TOL64
+    assert rel(res.theta_combined, meta["theta_combined"]) <= TOL64
+    U = pcb.normalized_ranks(X, pcb.partition(10000, 10).offsets, ctx=ctx)
+    import hashlib
+    assert hashlib.sha256(U.u1.tobytes() + U.u2.tobytes()).hexdigest() == meta["ranks_sha256"]
