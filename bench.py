@@ -1,0 +1,371 @@
+"""Benchmark: copula fit throughput (points/s, fp64) at n=1e9 per family on
+1..8 B200s — BASELINE.json metric, configs[4] (C5) workload.
+
+One step = the full hot path for Gaussian(rho=0.5), Frank(theta=5) and
+Gumbel(theta=2), each on its own n=1e9-point sample split into K=8000
+contiguous subsets of 125,000: per-subset bit-exact ranks ->
+Newton MPL fit -> asymptotic variance -> (N>1: NCCL all-gather of the
+per-subset records) -> inverse-variance combine on device.
+
+  value : 3e9 points / device time of one step, inputs resident in HBM
+          (max over ranks; CUDA events on the library's stream)
+  e2e   : the same metric through the C-ABI (pcb_fit_blocks) with HOST
+          (pinned) buffers: H2D of the step's inputs and D2H of the records
+          are inside the timed region
+
+--impl reference times the reference CPU path (oracle/_ref: the reference
+headers compiled in place + the SPEC restatement of fit/variance/combine) on
+all host cores, on a bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FAMILIES = [("gaussian", 0, 0.5), ("frank", 1, 5.0), ("gumbel", 2, 2.0)]
+N_PER_FAMILY = 1_000_000_000
+K_SUBSETS = 8000
+BASE_SEED = 0x160905530
+METRIC = "copula fit throughput (points/sec, fp64) at n=1e9, 1/2/4/8 B200, % roofline"
+# SURVEY.md §8(d) frozen algorithmic FP64 instructions per point per theta candidate (F_fit)
+F_FIT = {"gaussian": 9, "frank": 175, "gumbel": 210}
+B_PASS = 16  # bytes per point per likelihood pass (fp64 pair)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=N_PER_FAMILY, help="points per family (default 1e9)")
+    p.add_argument("--subsets", type=int, default=K_SUBSETS)
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (profiling runs)")
+    p.add_argument("--cpu-subsets", type=int, default=48, help="subsets per family in the CPU baseline sample")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_reference(args, steps, warmup, subsets_per_step):
+    """Reference CPU path on a bounded sample: per step, `subsets_per_step`
+    subsets of the C5 shape (125,000 points) per family, fitted by
+    oracle/_ref (reference headers + SPEC driver) on all host cores."""
+    from oracle.oracle import oracle_lib, ref_lib
+    orc = oracle_lib()
+    lib = ref_lib()
+    kind = "reference" if lib is not None else "port"
+    lib = lib or orc
+    cores = os.cpu_count() or 1
+    q = args.n // args.subsets
+    data = []
+    for name, fam, th in FAMILIES:
+        off_full = np.arange(subsets_per_step + 1, dtype=np.uint64) * np.uint64(q)
+        # the first subsets_per_step subsets of the same C5 partition (same seeds as the GPU arm)
+        offs = np.arange(args.subsets + 1, dtype=np.uint64) * np.uint64(q)
+        offs[-1] = args.n
+        c1, c2 = orc.sample_blocks(fam, th, args.n, args.subsets, offs, 0, subsets_per_step, base_seed=BASE_SEED)
+        data.append((name, fam, c1, c2, off_full))
+    pts = sum(len(d[2]) for d in data)
+
+    def one_step():
+        for name, fam, c1, c2, off in data:
+            recs = lib.fit_blocks(fam, c1, c2, off, workers=cores)
+            lib.combine(recs)
+
+    for _ in range(warmup):
+        one_step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one_step()
+    dt = (time.perf_counter() - t0) / steps
+    return pts, dt, kind, cores
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    sub = max(1, args.cpu_subsets // 3)
+    pts, dt, kind, cores = cpu_reference(args, args.steps, args.warmup, sub)
+    v = pts / dt
+    sample = f"{sub} subsets x {args.n // args.subsets} points per family (3 families) per step, C5 partition, seeds of the GPU arm"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "points/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C5 (BASELINE configs[4]) bounded CPU sample", "n_per_family": args.n,
+                   "subsets": args.subsets, "families": [f"{n}:{t}" for n, _, t in FAMILIES]},
+        "cpu_baseline": {"value": v, "unit": "points/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_05530_b200 as pcb
+    from paper_1609_05530_b200 import _lib as L
+    from paper_1609_05530_b200.distributed import gather_records, shard_blocks
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    ctx = pcb.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    K, n = args.subsets, args.n
+    q = n // K
+    first, last = shard_blocks(K, world, rank)
+    row0 = first * q
+    row1 = n if last == K else last * q
+    rows = row1 - row0
+    kl = last - first
+    off = (np.arange(kl + 1, dtype=np.uint64) * np.uint64(q))
+    off[-1] = rows
+    offp = off.ctypes.data_as(__import__("ctypes").POINTER(__import__("ctypes").c_uint64))
+
+    fp64_peak = ctx.fp64_peak()
+    # inputs resident in HBM (generation is not timed)
+    cols = {}
+    for name, fam, th in FAMILIES:
+        c1 = torch.empty(rows, dtype=torch.float64, device="cuda")
+        c2 = torch.empty(rows, dtype=torch.float64, device="cuda")
+        ctx.check(ctx.lib.pcb_sample(ctx.ptr, fam, th, n, K, first, last, BASE_SEED, c1.data_ptr(), c2.data_ptr()))
+        cols[name] = (c1, c2)
+    recs = {name: torch.zeros((kl, 6), dtype=torch.int64, device="cuda") for name, _, _ in FAMILIES}
+    gathered = {}
+    comb = {name: L.CombinedC() for name, _, _ in FAMILIES}
+    stage_acc = {name: {} for name, _, _ in FAMILIES}
+
+    def step(accumulate):
+        for name, fam, th in FAMILIES:
+            c1, c2 = cols[name]
+            ctx.check(ctx.lib.pcb_fit_blocks(ctx.ptr, fam, 0, c1.data_ptr(), c2.data_ptr(), rows, offp, kl,
+                                             recs[name].data_ptr()))
+            if accumulate:
+                for k, v in ctx.stage_times().items():
+                    stage_acc[name][k] = stage_acc[name].get(k, 0.0) + v
+            full = gather_records(recs[name], K) if world > 1 else recs[name]
+            gathered[name] = full
+            ctx.check(ctx.lib.pcb_combine(ctx.ptr, full.data_ptr(), K, None, __import__("ctypes").byref(comb[name])))
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launch_count() - launches0
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    total_points = n * len(FAMILIES)
+    value = total_points / (ms * 1e-3)
+
+    # roofline of the dominant kernel (the Newton likelihood pass, k_lik)
+    res = {}
+    for name, fam, th in FAMILIES:
+        arr = gathered[name].cpu().numpy().view(np.uint8).reshape(K, 48)
+        iters = arr[:, 32:36].copy().view(np.int32).ravel()
+        conv = arr[:, 36:40].copy().view(np.int32).ravel()
+        res[name] = {"theta_combined": comb[name].theta_combined, "blocks_used": int(comb[name].blocks_used),
+                     "mean_passes": float(iters.mean()), "converged": int(conv.sum())}
+    kernels = {}
+    for name, fam, th in FAMILIES:
+        sa = stage_acc[name]
+        steps = args.steps
+        kms = sa.get("lik_kernel_ms", 0.0) / steps
+        nl = sa.get("lik_launches", 0.0) / steps
+        passes = res[name]["mean_passes"]
+        entry = {"stage_ms": {k: v / steps for k, v in sa.items()}}
+        if kms > 0:
+            instr = F_FIT[name] * rows * passes  # algorithmic FP64 instructions (frozen F_fit) per step
+            entry["lik"] = {"ms": kms, "launches": nl, "avg_launch_ms": kms / max(nl, 1),
+                            "fp64_instr_per_s": instr / (kms * 1e-3), "hbm_gbs": B_PASS * rows * passes / (kms * 1e-3) / 1e9}
+        kernels[name] = entry
+    dom = max((k for k in kernels if "lik" in kernels[k]), key=lambda k: kernels[k]["lik"]["ms"], default=None)
+    roof = None
+    if dom:
+        lk = kernels[dom]["lik"]
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "lik_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(dom)
+            except Exception:
+                traffic = None
+        roof = {"bound": "fp64", "kernel": f"k_lik<{dom}, double2>", "achieved": lk["fp64_instr_per_s"] / 1e12,
+                "peak": fp64_peak / 1e12, "unit": "T FP64-instr/s", "frac": lk["fp64_instr_per_s"] / fp64_peak,
+                "peak_source": "measured live: DFMA-loop microbenchmark (pcb_measure_fp64_peak)",
+                "traffic": traffic, "algorithmic_per_point": F_FIT[dom],
+                "hbm_frac": lk["hbm_gbs"] / 6547.2}
+
+    # ------------------------------------------------------------ e2e
+    e2e = None
+    if not args.no_e2e:
+        del cols
+        torch.cuda.empty_cache()
+        host = {}
+        for name, fam, th in FAMILIES:
+            h1 = torch.empty(rows, dtype=torch.float64, pin_memory=True)
+            h2 = torch.empty(rows, dtype=torch.float64, pin_memory=True)
+            ctx.check(ctx.lib.pcb_sample(ctx.ptr, fam, th, n, K, first, last, BASE_SEED, h1.data_ptr(), h2.data_ptr()))
+            host[name] = (h1, h2)
+        hrec = {name: np.zeros((kl, 6), np.int64) for name, _, _ in FAMILIES}
+
+        def e2e_step():
+            for name, fam, th in FAMILIES:
+                h1, h2 = host[name]
+                ctx.check(ctx.lib.pcb_fit_blocks(ctx.ptr, fam, 0, h1.data_ptr(), h2.data_ptr(), rows, offp, kl,
+                                                 hrec[name].ctypes.data))
+                if world > 1:
+                    full = gather_records(torch.from_numpy(hrec[name]).cuda(), K)
+                    ctx.check(ctx.lib.pcb_combine(ctx.ptr, full.data_ptr(), K, None,
+                                                  __import__("ctypes").byref(comb[name])))
+                else:
+                    ctx.check(ctx.lib.pcb_combine(ctx.ptr, hrec[name].ctypes.data, K, None,
+                                                  __import__("ctypes").byref(comb[name])))
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": total_points / dt, "unit": "points/s", "h2d_bytes_per_step": int(16 * n * len(FAMILIES)),
+               "d2h_bytes_per_step": int(48 * K * len(FAMILIES)), "ms_per_step": dt * 1e3,
+               "timing": "host wall clock around the synchronous C-ABI calls (max over ranks)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            sub = max(1, args.cpu_subsets // 3)
+            pts, dt, kind, cores = cpu_reference(args, 1, 0, sub)
+            cpu = {"value": pts / dt, "unit": "points/s", "cores": cores, "kind": kind,
+                   "sample": f"{sub} subsets x {q} points per family (3 families), C5 partition, same seeds"}
+        except Exception as ex:  # never fail the GPU line on the baseline leg
+            cpu = {"value": None, "unit": "points/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5 (BASELINE configs[4]): Gaussian rho=0.5 + Frank theta=5 + Gumbel theta=2, "
+                                   "n=1e9 fp64 pairs per family, K=8000 subsets of 125000, rank->fit->variance->gather->combine",
+                       "n_per_family": n, "subsets": K, "subset_rows": q, "parallelism": f"dp{world} (subset shards)",
+                       "l2": "inputs (16 GB per family) exceed the 126 MB L2; no flush needed"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk, "kernels": kernels, "results": res,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    ctx.close()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -247,8 +247,8 @@ def validate_data(X: DataMatrix) -> None:  # pseudo_obs.hpp:30-37
 
 def normalized_ranks(X: DataMatrix, segments: Optional[Sequence[int]] = None, ctx: Context = None) -> PseudoSample:
     """pseudo_obs.hpp:71-77; `segments` (offsets) ranks each block locally."""
-    ctx = ctx or default_context()
     validate_data(X)
+    ctx = ctx or default_context()
     c1, c2 = _f64(X.col1), _f64(X.col2)
     n = len(c1)
     u1, u2 = _like(c1, n), _like(c2, n)
@@ -337,10 +337,10 @@ def partition(X_or_rows, M: int, scheme=Scheme.Contiguous) -> Partition:
 
 def combine(results: Sequence[FitResult], ctx: Context = None) -> CombinedResult:
     """SPEC.md:284-292, on device."""
-    ctx = ctx or default_context()
     k = len(results)
     if k == 0:
         raise ValueError("combine: empty input")
+    ctx = ctx or default_context()
     arr = (L.FitResultC * k)()
     for i, r in enumerate(results):
         arr[i] = L.FitResultC(r.theta_hat, r.sigma2, r.loglik, r.n, r.iterations, int(r.converged),
@@ -368,8 +368,10 @@ def fit_parallel(family, X: DataMatrix, M: int, workers: Optional[int] = None, s
                  precision=Precision.fp64, ctx: Context = None) -> CombinedResult:
     """SPEC.md:293-301. `workers` is accepted for signature compatibility:
     blocks run on the GPU's SMs (the result is identical for any value)."""
-    ctx = ctx or default_context()
     validate_data(X)
+    if M < 1:
+        raise ValueError("partition: need M >= 1")
+    ctx = ctx or default_context()
     c1, c2 = _f64(X.col1), _f64(X.col2)
     n = len(c1)
     per = (L.FitResultC * M)()
