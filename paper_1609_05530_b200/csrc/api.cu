@@ -136,9 +136,7 @@ struct RankBufs {
 
 RankBufs rank_buffers(pcb::Ctx& c, uint64_t n_rows, uint64_t n_seg) {
     RankBufs b;
-    b.r.r2 = c.ws.get_t<uint32_t>("pipe.r2", 2 * n_rows);
-    b.r.pos = c.ws.get_t<uint32_t>("pipe.pos", 2 * n_rows);
-    b.r.lt = c.ws.get_t<uint32_t>("pipe.lt", 2 * n_rows);
+    b.r.rp = c.ws.get_t<unsigned long long>("pipe.rp", 2 * n_rows);
     b.bad = c.ws.get_t<int32_t>("pipe.bad", n_seg);
     PCB_CUDA(cudaMemsetAsync(b.bad, 0, n_seg * sizeof(int32_t), c.stream));
     return b;
@@ -169,9 +167,7 @@ void pipeline_blocks(pcb::Ctx& c, int fam, int prec, const double* d1, const dou
     io.precision = prec;
     io.n_rows = n_rows;
     io.off = off;
-    io.r2 = rb.r.r2;
-    io.pos = rb.r.pos;
-    io.lt = rb.r.lt;
+    io.rp = rb.r.rp;
     io.bad = rb.bad;
     pcb::run_fit(c, io, d_out);
     finish_stage_times(c);
@@ -268,7 +264,7 @@ int pcb_normalized_ranks(pcb_context* ctx, const double* col1, const double* col
         for (int32_t b : bad)
             if (b) throw pcb::Error(PCB_E_DOMAIN, "data matrix: non-finite value");  // pseudo_obs.hpp:36
         DevOut<double> o1(c, u1, n_rows, "u1"), o2(c, u2, n_rows, "u2");
-        pcb::ranks_to_u(c, rb.r.r2, n_rows, off, o1.dev, o2.dev);
+        pcb::ranks_to_u(c, rb.r.rp, n_rows, off, o1.dev, o2.dev);
         o1.finish(c);
         o2.finish(c);
         PCB_CUDA(cudaStreamSynchronize(c.stream));
@@ -321,8 +317,7 @@ int pcb_fit(pcb_context* ctx, int family, int precision, const double* u1, const
         io.off = off;
         io.u1 = d1;
         io.u2 = d2;
-        io.pos = rb.r.pos;
-        io.lt = rb.r.lt;
+        io.rp = rb.r.rp;
         DevOut<pcb_fit_result> o(c, out, n_seg, "fit");
         pcb::run_fit(c, io, o.dev);
         finish_stage_times(c);
@@ -360,8 +355,7 @@ int pcb_asymptotic_variance(pcb_context* ctx, int family, const double* theta_ha
         io.off = off;
         io.u1 = d1;
         io.u2 = d2;
-        io.pos = rb.r.pos;
-        io.lt = rb.r.lt;
+        io.rp = rb.r.rp;
         io.theta_in = dth;
         io.do_fit = false;
         auto* rec = c.ws.get_t<pcb_fit_result>("var.rec", n_seg);

@@ -89,4 +89,64 @@ __device__ __forceinline__ double key_value(uint64_t k) {
     return __longlong_as_double(static_cast<long long>(b));
 }
 
+// ------------------------------------------------------ tile reductions
+// Fit / variance kernels map one CTA to one tile of FTILE points that never
+// straddles a segment (Seg::tile0 = first tile of the segment).
+constexpr int FT = 256;  // threads per tile CTA
+constexpr int PPT = 8;   // points per thread per tile
+constexpr uint32_t FTILE = FT * PPT;
+
+// Stores this tile's NV partial sums; the segment's last-arriving tile sums
+// all the segment's tile partials in tile order (deterministic: fixed
+// per-tile trees, fixed final order, no floating-point atomics). Returns
+// true in the last tile, with the segment totals in thread 0's v[].
+template <int NV>
+__device__ bool tile_reduce(double (&v)[NV], double* sh, double* partials, unsigned* tickets, const Seg& S, int m,
+                            uint32_t tile) {
+    block_sum<NV>(v, sh);
+    __shared__ bool s_last;
+    const uint32_t nt = (S.n + FTILE - 1) / FTILE;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) partials[static_cast<size_t>(tile) * NV + k] = v[k];
+        __threadfence();
+        const unsigned ticket = atomicAdd(tickets + m, 1u);
+        s_last = ticket == nt - 1;
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    double acc[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+    for (uint32_t q = threadIdx.x; q < nt; q += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] += __ldcg(partials + static_cast<size_t>(S.tile0 + q) * NV + k);
+    }
+    block_sum<NV>(acc, sh);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = acc[k];
+    if (threadIdx.x == 0) tickets[m] = 0u;
+    return true;
+}
+
+__host__ __device__ __forceinline__ unsigned long long pack_rank(uint32_t r2, uint32_t pos) {
+    return static_cast<unsigned long long>(r2) | (static_cast<unsigned long long>(pos) << 32);
+}
+__host__ __device__ __forceinline__ uint32_t rank_r2(unsigned long long rp) { return static_cast<uint32_t>(rp); }
+__host__ __device__ __forceinline__ uint32_t rank_pos(unsigned long long rp) { return static_cast<uint32_t>(rp >> 32); }
+
+// (u, v) of a point: the caller's pseudo-observations, or exactly
+// normalized_rank_column's value from the packed rank (pseudo_obs.hpp:59-60).
+__device__ __forceinline__ void point_u(const unsigned long long* rp, const double* u1, const double* u2,
+                                        uint64_t n_rows, uint64_t row, double scale, double& u, double& v) {
+    if (u1) {
+        u = u1[row];
+        v = u2[row];
+    } else {
+        u = __dmul_rn(0.5 * static_cast<double>(rank_r2(rp[row])), scale);
+        v = __dmul_rn(0.5 * static_cast<double>(rank_r2(rp[n_rows + row])), scale);
+    }
+}
+
 }  // namespace pcb

@@ -328,10 +328,10 @@ __device__ __forceinline__ void gumbel_sh_f(float lx, float ly, const GumbelThet
     h = -wtt - 2.0f * r * g.inv_t2 + 2.0f * lnS * g.inv_t3 + g.c1t * rt + (wtt * gg - wt1 * wt1) * rg * rg;
 }
 
-// Full evaluation at (u, v) for the variance pass (copula.hpp:199-254).
-__device__ __forceinline__ PointFull gumbel_full(double u, double v, const GumbelTheta& g) {
-    const double x = -log(u), y = -log(v);
-    const double lx = log(x), ly = log(y);
+// Full evaluation for the variance pass (copula.hpp:199-254), from
+// x = -ln u, y = -ln v and their logs.
+__device__ __forceinline__ PointFull gumbel_full_core(double u, double v, double x, double y, double lx, double ly,
+                                                      const GumbelTheta& g) {
     const double a = g.t * lx, b = g.t * ly;
     const double m = fmax(a, b);
     const double ea = exp(a - m), eb = exp(b - m);
@@ -369,6 +369,16 @@ __device__ __forceinline__ PointFull gumbel_full(double u, double v, const Gumbe
         p.cross2 = -cy / v;
     }
     return p;
+}
+
+__device__ __forceinline__ PointFull gumbel_full(double u, double v, const GumbelTheta& g) {
+    const double x = -log(u), y = -log(v);
+    return gumbel_full_core(u, v, x, y, log(x), log(y), g);
+}
+
+// from the hoisted (ln x, ln y) pair of the prepare pass
+__device__ __forceinline__ PointFull gumbel_full_l(double u, double v, double lx, double ly, const GumbelTheta& g) {
+    return gumbel_full_core(u, v, exp(lx), exp(ly), lx, ly, g);
 }
 
 // log c only (pseudo_loglik API), any family; u, v already clamped.

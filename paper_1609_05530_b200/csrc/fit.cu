@@ -1,23 +1,20 @@
-// K2 lik_reduce + batched Newton, K3-K5 asymptotic variance, on sm_100a.
+// K2 lik_reduce + batched safeguarded Newton on sm_100a.
 //
-// Replaces the reference's absent mpl_estimator:
-//   fit                 SPEC.md:216-224, 242-244 — here: every block's root of
-//                       the pseudo-score equation, all blocks in lockstep, one
-//                       fused score+Hessian reduction launch per Newton pass
-//   asymptotic_variance SPEC.md:225-233, 246 — one pass for the per-point
-//                       terms with cross derivatives scattered by stable rank,
-//                       a per-(block, column) suffix scan (the W-term), and a
-//                       final reduction of M-hat
-// Data layout (HBM): the rank stage leaves per column r2/pos/lt u32 arrays
-// ([2][n_rows]); the prepare pass writes the theta-independent per-point
-// pair T (double2 or float2, n_rows) the Newton passes stream:
-//   Gaussian : nothing — the fit reduces to Sxy and Sss (sufficient stats)
+// Replaces the reference's absent mpl_estimator `fit` (SPEC.md:216-224,
+// 242-244): every block's theta-hat is the root of its pseudo-score
+// equation, all blocks in lockstep, one fused score+Hessian reduction launch
+// per Newton pass (the asymptotic variance is variance.cu).
+// Data layout (HBM): the rank stage leaves packed (r2|pos) u64 per point and
+// column ([2][n_rows]); the prepare pass writes the theta-independent
+// per-point pair T (double2, or float2 on the fp32 likelihood path) that the
+// Newton passes stream:
+//   Gaussian : (x, y) = (Phi^-1(u), Phi^-1(v)); the fit itself reduces to the
+//              sufficient statistics Sxy, Sss (no Newton data pass); T feeds
+//              the variance pass
 //   Frank    : (u, v)   (fp32: edge-encoded, see frank_edge)
 //   Gumbel   : (ln(-ln u), ln(-ln v))   (copula.hpp:201-204, hoisted)
-// Reductions are deterministic: fixed tiles (never straddling a block),
-// fixed per-tile trees, and the last-arriving tile of a block sums the tile
-// partials in tile order — no floating-point atomics anywhere, so results do
-// not depend on scheduling, on the number of GPUs, or on the run.
+// Reductions are deterministic (common.cuh tile_reduce): no floating-point
+// atomics, so results do not depend on scheduling, the GPU count or the run.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -29,9 +26,6 @@
 namespace pcb {
 namespace {
 
-constexpr int FT = 256;        // threads per fit block
-constexpr int PPT = 8;         // points per thread per tile
-constexpr uint32_t FTILE = FT * PPT;
 constexpr int kMaxPasses = 64;
 constexpr double kTol64 = 2e-8;  // Newton step tolerance (relative); error after ~C*tol^2
 constexpr double kTol32 = 1e-6;
@@ -115,22 +109,9 @@ __device__ void newton_update(BlockState& s, int fam, double S, double H, double
     }
 }
 
-__device__ __forceinline__ void point_u(const uint32_t* r2, const double* u1, const double* u2, uint64_t n_rows,
-                                        uint64_t row, double scale, double& u, double& v) {
-    if (r2) {  // exactly normalized_rank_column's value (pseudo_obs.hpp:59-60)
-        u = __dmul_rn(0.5 * static_cast<double>(r2[row]), scale);
-        v = __dmul_rn(0.5 * static_cast<double>(r2[n_rows + row]), scale);
-    } else {
-        u = u1[row];
-        v = u2[row];
-    }
-}
-
 // Edge encoding for fp32 Frank inputs: p = u (u <= 1/2) or -(1-u) (u > 1/2),
 // computed in fp64, so both u and 1-u keep full fp32 relative precision.
-__device__ __forceinline__ float frank_edge(double u) {
-    return static_cast<float>(u <= 0.5 ? u : -(1.0 - u));
-}
+__device__ __forceinline__ float frank_edge(double u) { return static_cast<float>(u <= 0.5 ? u : -(1.0 - u)); }
 __device__ __forceinline__ void frank_unedge(float p, float& val, float& comp) {
     if (p >= 0.0f) {
         val = p;
@@ -139,39 +120,6 @@ __device__ __forceinline__ void frank_unedge(float p, float& val, float& comp) {
         val = 1.0f + p;
         comp = -p;
     }
-}
-
-// Last-tile-of-block reduction helper: stores this tile's NV partials; the
-// block's last tile sums all its tiles' partials in tile order.
-template <int NV>
-__device__ bool tile_reduce(double (&v)[NV], double* sh, double* partials, unsigned* tickets, const Seg& S, int m,
-                            uint32_t tile) {
-    block_sum<NV>(v, sh);
-    __shared__ bool s_last;
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 0; k < NV; ++k) partials[static_cast<size_t>(tile) * NV + k] = v[k];
-        __threadfence();
-        const uint32_t nt = (S.n + FTILE - 1) / FTILE;
-        const unsigned ticket = atomicAdd(tickets + m, 1u);
-        s_last = ticket == nt - 1;
-    }
-    __syncthreads();
-    if (!s_last) return false;
-    __threadfence();
-    const uint32_t nt = (S.n + FTILE - 1) / FTILE;
-    double acc[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-    for (uint32_t q = threadIdx.x; q < nt; q += FT) {
-#pragma unroll
-        for (int k = 0; k < NV; ++k) acc[k] += __ldcg(partials + static_cast<size_t>(S.tile0 + q) * NV + k);
-    }
-    block_sum<NV>(acc, sh);
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = acc[k];
-    if (threadIdx.x == 0) tickets[m] = 0u;
-    return true;
 }
 
 __global__ void k_init_state(BlockState* st, const Seg* segs, int nseg, const int32_t* bad, unsigned* running,
@@ -197,15 +145,18 @@ __global__ void k_init_state(BlockState* st, const Seg* segs, int nseg, const in
 }
 
 // Prepare pass: theta-independent per-point pair + init statistics; the
-// block's last tile computes the starting theta (Gaussian: solves the fit).
+// segment's last tile computes the starting theta (Gaussian: solves the fit).
+// with_fit == 0 (variance-only API): only T is written.
 template <int FAM, class TO>
-__global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs, int nseg, const uint32_t* r2,
-                                               const double* u1, const double* u2, uint64_t n_rows, TO* T,
-                                               double* partials, unsigned* tickets, unsigned* running, int fp32) {
+__global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs, int nseg,
+                                               const unsigned long long* rp, const double* u1, const double* u2,
+                                               uint64_t n_rows, TO* T, double* partials, unsigned* tickets,
+                                               unsigned* running, int with_fit) {
     const uint32_t tile = blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
-    if (st[m].status != kRunning) return;
+    const int32_t status = st[m].status;
+    if (with_fit ? status != kRunning : status != kConverged) return;
     const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);
     const uint32_t base = (tile - S.tile0) * FTILE;
     double v[2] = {0.0, 0.0};
@@ -215,23 +166,28 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
         if (i >= S.n) break;
         const uint64_t row = S.begin + i;
         double u, w;
-        point_u(r2, u1, u2, n_rows, row, scale, u, w);
+        point_u(rp, u1, u2, n_rows, row, scale, u, w);
+        u = clamp_unit(u);
+        w = clamp_unit(w);
         if (FAM == kGaussian) {
-            const double x = dev_phi_inv(clamp_unit(u)), y = dev_phi_inv(clamp_unit(w));
+            const double x = dev_phi_inv(u), y = dev_phi_inv(w);
             v[0] += x * y;
             v[1] += x * x + y * y;
+            T[row] = TO{static_cast<decltype(TO::x)>(x), static_cast<decltype(TO::x)>(y)};
         } else {
             v[0] += u * w;
             if (FAM == kFrank) {
-                if (sizeof(TO) == 8) T[row] = TO{static_cast<decltype(TO::x)>(frank_edge(u)),
-                                                 static_cast<decltype(TO::x)>(frank_edge(w))};
-                else T[row] = TO{static_cast<decltype(TO::x)>(u), static_cast<decltype(TO::x)>(w)};
+                if (sizeof(TO) == 8)
+                    T[row] = TO{static_cast<decltype(TO::x)>(frank_edge(u)), static_cast<decltype(TO::x)>(frank_edge(w))};
+                else
+                    T[row] = TO{static_cast<decltype(TO::x)>(u), static_cast<decltype(TO::x)>(w)};
             } else {
-                const double lx = log(-log(clamp_unit(u))), ly = log(-log(clamp_unit(w)));
+                const double lx = log(-log(u)), ly = log(-log(w));
                 T[row] = TO{static_cast<decltype(TO::x)>(lx), static_cast<decltype(TO::x)>(ly)};
             }
         }
     }
+    if (!with_fit) return;
     __shared__ double sh[(FT / 32) * 2];
     if (!tile_reduce<2>(v, sh, partials, tickets, S, m, tile)) return;
     if (threadIdx.x != 0) return;
@@ -389,123 +345,6 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
     }
 }
 
-// Variance pass 1 at theta-hat: log c, score, Hessian, cross terms; the
-// cross terms are scattered to their block's stable sorted positions.
-template <int FAM>
-__global__ void __launch_bounds__(FT) k_var_terms(BlockState* st, const Seg* segs, int nseg, const uint32_t* r2,
-                                                 const double* u1, const double* u2, const uint32_t* pos,
-                                                 uint64_t n_rows, double* score, double* A, double* partials,
-                                                 unsigned* tickets) {
-    const uint32_t tile = blockIdx.x;
-    const int m = seg_of_tile(segs, nseg, tile);
-    const Seg S = segs[m];
-    const int32_t status = st[m].status;
-    if (status != kConverged) return;
-    const double theta = st[m].theta;
-    const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);
-    const uint32_t base = (tile - S.tile0) * FTILE;
-    double v[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int k = 0; k < PPT; ++k) {
-        const uint32_t i = base + k * FT + threadIdx.x;
-        if (i >= S.n) break;
-        const uint64_t row = S.begin + i;
-        double u, w;
-        point_u(r2, u1, u2, n_rows, row, scale, u, w);
-        u = clamp_unit(u);
-        w = clamp_unit(w);
-        PointFull p;
-        if (FAM == kGaussian) p = gauss_full(dev_phi_inv(u), dev_phi_inv(w), GaussTheta(theta));
-        else if (FAM == kFrank) p = frank_full(u, w, FrankTheta(theta));
-        else p = gumbel_full(u, w, GumbelTheta(theta));
-        score[row] = p.score;
-        A[S.begin + pos[row]] = p.cross1;
-        A[n_rows + S.begin + pos[n_rows + row]] = p.cross2;
-        v[0] += p.hess;
-        v[1] += u * p.cross1;
-        v[2] += w * p.cross2;
-        v[3] += clip_log(p.logc);
-    }
-    __shared__ double sh[(FT / 32) * 4];
-    if (!tile_reduce<4>(v, sh, partials, tickets, S, m, tile)) return;
-    if (threadIdx.x == 0) {
-        st[m].info_sum = v[0];
-        st[m].c1 = v[1];
-        st[m].c2 = v[2];
-        st[m].loglik = v[3];
-    }
-}
-
-// In-place inclusive suffix sum of A over each (block, column) segment; one
-// CTA per segment, fixed chunking (deterministic).
-__global__ void __launch_bounds__(1024) k_suffix(const BlockState* st, const Seg* segs, int nseg, uint64_t n_rows,
-                                                double* A) {
-    const int m = blockIdx.x % nseg;
-    const int col = blockIdx.x / nseg;
-    if (st[m].status != kConverged) return;
-    const Seg S = segs[m];
-    double* a = A + static_cast<uint64_t>(col) * n_rows + S.begin;
-    const uint32_t n = S.n;
-    const uint32_t chunk = (n + blockDim.x - 1) / blockDim.x;
-    const uint32_t b0 = min(n, threadIdx.x * chunk), b1 = min(n, b0 + chunk);
-    double local = 0.0;
-    for (uint32_t q = b1; q-- > b0;) local += a[q];
-    // exclusive suffix scan of the chunk totals (chunks to the right)
-    __shared__ double s_tot[1024];
-    s_tot[threadIdx.x] = local;
-    __syncthreads();
-    // Hillis-Steele suffix scan in shared memory (fixed order)
-    for (int o = 1; o < static_cast<int>(blockDim.x); o <<= 1) {
-        double add = 0.0;
-        if (threadIdx.x + o < blockDim.x) add = s_tot[threadIdx.x + o];
-        __syncthreads();
-        s_tot[threadIdx.x] += add;
-        __syncthreads();
-    }
-    double run = threadIdx.x + 1 < blockDim.x ? s_tot[threadIdx.x + 1] : 0.0;
-    for (uint32_t q = b1; q-- > b0;) {
-        run += a[q];
-        a[q] = run;
-    }
-}
-
-// Variance pass 2: W_ji = (suffix at the tie run's first position - C_j)/n,
-// M-hat = mean (score + W_1 + W_2)^2, sigma2 = M/I^2/n.
-__global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* segs, int nseg, const uint32_t* lt,
-                                                 uint64_t n_rows, const double* score, const double* A,
-                                                 double* partials, unsigned* tickets) {
-    const uint32_t tile = blockIdx.x;
-    const int m = seg_of_tile(segs, nseg, tile);
-    const Seg S = segs[m];
-    if (st[m].status != kConverged) return;
-    const double n = static_cast<double>(S.n);
-    const double c1 = st[m].c1, c2 = st[m].c2;
-    const uint32_t base = (tile - S.tile0) * FTILE;
-    double v[1] = {0.0};
-    for (int k = 0; k < PPT; ++k) {
-        const uint32_t i = base + k * FT + threadIdx.x;
-        if (i >= S.n) break;
-        const uint64_t row = S.begin + i;
-        const double w1 = (A[S.begin + lt[row]] - c1) / n;
-        const double w2 = (A[n_rows + S.begin + lt[n_rows + row]] - c2) / n;
-        const double z = score[row] + w1 + w2;
-        v[0] += z * z;
-    }
-    __shared__ double sh[FT / 32];
-    if (!tile_reduce<1>(v, sh, partials, tickets, S, m, tile)) return;
-    if (threadIdx.x == 0) {
-        BlockState s = st[m];
-        const double info = -s.info_sum / n;
-        if (!(info > 0.0)) {
-            s.status = kInfoNonPos;
-            s.sigma2 = NAN;
-        } else {
-            const double mhat = v[0] / n;
-            s.sigma2 = mhat / (info * info) / n;
-        }
-        st[m] = s;
-    }
-}
-
 struct RecordOut {  // == pcb_fit_result
     double theta_hat, sigma2, loglik;
     uint64_t n;
@@ -609,13 +448,13 @@ uint32_t ftiles(uint64_t n) { return static_cast<uint32_t>((n + FTILE - 1) / FTI
 
 template <int FAM>
 void launch_prepare(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, const FitIO& io, void* T,
-                    double* part, unsigned* tick, unsigned* running) {
-    if (io.precision == 1 && FAM != kGaussian)
-        k_prepare<FAM, float2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.r2, io.u1, io.u2, io.n_rows,
-                                                          static_cast<float2*>(T), part, tick, running, 1);
+                    bool fp32T, double* part, unsigned* tick, unsigned* running, int with_fit) {
+    if (fp32T)
+        k_prepare<FAM, float2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.rp, io.u1, io.u2, io.n_rows,
+                                                          static_cast<float2*>(T), part, tick, running, with_fit);
     else
-        k_prepare<FAM, double2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.r2, io.u1, io.u2, io.n_rows,
-                                                           static_cast<double2*>(T), part, tick, running, 0);
+        k_prepare<FAM, double2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.rp, io.u1, io.u2, io.n_rows,
+                                                           static_cast<double2*>(T), part, tick, running, with_fit);
     c.count_launch();
 }
 
@@ -628,14 +467,6 @@ void launch_lik(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, 
     else
         k_lik<FAM, double2><<<tiles, FT, 0, c.stream>>>(st, segs, K, static_cast<const double2*>(T), part, tick,
                                                         running);
-    c.count_launch();
-}
-
-template <int FAM>
-void launch_var(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, const FitIO& io, double* score,
-                double* A, double* part, unsigned* tick) {
-    k_var_terms<FAM><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.r2, io.u1, io.u2, io.pos, io.n_rows, score, A,
-                                                 part, tick);
     c.count_launch();
 }
 
@@ -675,55 +506,58 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
     PCB_CUDA(cudaMemcpyAsync(d_segs, segs.data(), K * sizeof(Seg), cudaMemcpyHostToDevice, s));
     PCB_CUDA(cudaMemsetAsync(tick, 0, K * sizeof(unsigned), s));
     PCB_CUDA(cudaMemsetAsync(running, 0, sizeof(unsigned), s));
+    cudaEvent_t* ev = c.ev;
+    PCB_CUDA(cudaEventRecord(ev[1], s));
     k_init_state<<<(K + 127) / 128, 128, 0, s>>>(st, d_segs, K, io.bad, running, io.theta_in);
     c.count_launch();
     const int fam = io.family;
-    if (tiles == 0) return;
-    cudaEvent_t* ev = c.ev;
-    PCB_CUDA(cudaEventRecord(ev[1], s));
-    if (io.do_fit) {
-        void* T = nullptr;
-        if (fam != kGaussian)
-            T = c.ws.get("fit.T", io.n_rows * (io.precision == 1 ? sizeof(float2) : sizeof(double2)));
-        if (fam == kGaussian) launch_prepare<kGaussian>(c, tiles, st, d_segs, K, io, T, part, tick, running);
-        else if (fam == kFrank) launch_prepare<kFrank>(c, tiles, st, d_segs, K, io, T, part, tick, running);
-        else launch_prepare<kGumbel>(c, tiles, st, d_segs, K, io, T, part, tick, running);
-        PCB_CUDA(cudaEventRecord(ev[2], s));
-        float lik_ms = 0.0f;
-        int lik_launches = 0;
-        if (fam != kGaussian) {
-            for (int pass = 0; pass < kMaxPasses; ++pass) {
-                PCB_CUDA(cudaEventRecord(ev[6], s));
-                if (fam == kFrank) launch_lik<kFrank>(c, tiles, st, d_segs, K, io.precision, T, part, tick, running);
-                else launch_lik<kGumbel>(c, tiles, st, d_segs, K, io.precision, T, part, tick, running);
-                PCB_CUDA(cudaEventRecord(ev[7], s));
-                PCB_CUDA(cudaMemcpyAsync(h_running, running, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-                PCB_CUDA(cudaStreamSynchronize(s));
-                float ms = 0.0f;
-                PCB_CUDA(cudaEventElapsedTime(&ms, ev[6], ev[7]));
-                lik_ms += ms;
-                ++lik_launches;
-                if (*h_running == 0) break;
-            }
-        }
-        PCB_CUDA(cudaEventRecord(ev[3], s));
-        c.stage_ms[5] = lik_ms;
-        c.stage_ms[6] = lik_launches;
-    } else {
-        PCB_CUDA(cudaEventRecord(ev[2], s));
-        PCB_CUDA(cudaEventRecord(ev[3], s));
-        c.stage_ms[5] = 0.0;
-        c.stage_ms[6] = 0;
+    // T: fp32 only for the Archimedean fp32 likelihood path; the Gaussian
+    // (x, y) pair is always fp64 (it only feeds the variance pass).
+    const bool fp32T = io.precision == 1 && fam != kGaussian;
+    void* T = c.ws.get("fit.T", io.n_rows * (fp32T ? sizeof(float2) : sizeof(double2)));
+    if (tiles > 0) {
+        const int with_fit = io.do_fit ? 1 : 0;
+        if (fam == kGaussian) launch_prepare<kGaussian>(c, tiles, st, d_segs, K, io, T, fp32T, part, tick, running, with_fit);
+        else if (fam == kFrank) launch_prepare<kFrank>(c, tiles, st, d_segs, K, io, T, fp32T, part, tick, running, with_fit);
+        else launch_prepare<kGumbel>(c, tiles, st, d_segs, K, io, T, fp32T, part, tick, running, with_fit);
     }
-    if (io.do_variance) {
-        auto* score = c.ws.get_t<double>("fit.score", io.n_rows);
-        auto* A = c.ws.get_t<double>("fit.A", 2 * io.n_rows);
-        if (fam == kGaussian) launch_var<kGaussian>(c, tiles, st, d_segs, K, io, score, A, part, tick);
-        else if (fam == kFrank) launch_var<kFrank>(c, tiles, st, d_segs, K, io, score, A, part, tick);
-        else launch_var<kGumbel>(c, tiles, st, d_segs, K, io, score, A, part, tick);
-        k_suffix<<<2 * K, 1024, 0, s>>>(st, d_segs, K, io.n_rows, A);
-        k_var_final<<<tiles, FT, 0, s>>>(st, d_segs, K, io.lt, io.n_rows, score, A, part, tick);
-        c.count_launch(2);
+    PCB_CUDA(cudaEventRecord(ev[2], s));
+    float lik_ms = 0.0f;
+    int lik_launches = 0;
+    if (io.do_fit && fam != kGaussian && tiles > 0) {
+        for (int pass = 0; pass < kMaxPasses; ++pass) {
+            PCB_CUDA(cudaEventRecord(ev[6], s));
+            if (fam == kFrank) launch_lik<kFrank>(c, tiles, st, d_segs, K, io.precision, T, part, tick, running);
+            else launch_lik<kGumbel>(c, tiles, st, d_segs, K, io.precision, T, part, tick, running);
+            PCB_CUDA(cudaEventRecord(ev[7], s));
+            PCB_CUDA(cudaMemcpyAsync(h_running, running, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+            PCB_CUDA(cudaStreamSynchronize(s));
+            float ms = 0.0f;
+            PCB_CUDA(cudaEventElapsedTime(&ms, ev[6], ev[7]));
+            lik_ms += ms;
+            ++lik_launches;
+            if (*h_running == 0) break;
+        }
+    }
+    PCB_CUDA(cudaEventRecord(ev[3], s));
+    c.stage_ms[5] = lik_ms;
+    c.stage_ms[6] = lik_launches;
+    if (io.do_variance && tiles > 0) {
+        VarIO v;
+        v.family = fam;
+        v.n_rows = io.n_rows;
+        v.off = &io.off;
+        v.segs = d_segs;
+        v.h_segs = &segs;
+        v.tiles = tiles;
+        v.st = st;
+        v.rp = io.rp;
+        v.u1 = io.u1;
+        v.u2 = io.u2;
+        v.T64 = (fam == kGaussian || (fam == kGumbel && !fp32T)) ? static_cast<const double2*>(T) : nullptr;
+        v.partials = part;
+        v.tickets = tick;
+        run_variance(c, v);
     }
     PCB_CUDA(cudaEventRecord(ev[4], s));
     k_finalize<<<(K + 127) / 128, 128, 0, s>>>(st, K, static_cast<RecordOut*>(d_out), io.do_variance ? 1 : 0);

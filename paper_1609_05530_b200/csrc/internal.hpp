@@ -87,14 +87,13 @@ struct Ctx {
 };
 
 // ---------------------------------------------------------------- ranks
-// Segment-local bit-exact rank outputs, [2][n_rows] u32 each:
-//   r2  = (i+1)+(j+1), twice the 1-based average rank of the tie run i..j
-//   pos = unique stable sorted position (ties ordered by row index)
-//   lt  = i, the tie run's first sorted position
+// Segment-local bit-exact rank outputs, [2][n_rows] packed u64
+// (pack_rank in common.cuh):
+//   low 32  r2  = (i+1)+(j+1), twice the 1-based average rank of the tie run i..j
+//   high 32 pos = unique stable sorted position (ties ordered by row index)
+// A tie run is the set of sorted positions sharing one r2.
 struct RankOut {
-    uint32_t* r2;
-    uint32_t* pos;
-    uint32_t* lt;
+    unsigned long long* rp;
 };
 
 // Ranks both columns of every segment. `bad` (n_seg int32, device) is set
@@ -103,7 +102,7 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
                RankOut out, int32_t* d_bad);
 
 // u = (0.5*r2) * (1/(n_m+1)), bit-exact to normalized_rank_column
-void ranks_to_u(Ctx& c, const uint32_t* r2, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
+void ranks_to_u(Ctx& c, const unsigned long long* rp, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
                 double* u2);
 
 // ---------------------------------------------------------------- fit
@@ -112,12 +111,11 @@ struct FitIO {
     int precision = 0;
     uint64_t n_rows = 0;
     std::vector<uint64_t> off;  // host offsets (n_seg + 1)
-    // exactly one source of (u, v): explicit arrays or rank pairs
+    // packed ranks [2][n_rows] (always: the variance needs the stable
+    // positions); (u, v) come from u1/u2 when given, else from the ranks
+    const unsigned long long* rp = nullptr;
     const double* u1 = nullptr;
     const double* u2 = nullptr;
-    const uint32_t* r2 = nullptr;  // [2][n_rows]
-    const uint32_t* pos = nullptr;
-    const uint32_t* lt = nullptr;
     const int32_t* bad = nullptr;  // per segment, may be null
     const double* theta_in = nullptr;  // device: skip the fit, evaluate at these (variance API)
     bool do_fit = true;
@@ -127,6 +125,24 @@ struct FitIO {
 // Runs prepare -> init -> Newton passes -> variance; writes n_seg
 // pcb_fit_result-compatible records (device) into d_out.
 void run_fit(Ctx& c, const FitIO& io, void* d_out_records);
+
+// Asymptotic variance at each converged block's theta.
+struct VarIO {
+    int family = 0;
+    uint64_t n_rows = 0;
+    const std::vector<uint64_t>* off = nullptr;
+    const Seg* segs = nullptr;                  // device
+    const std::vector<Seg>* h_segs = nullptr;   // host copy
+    uint32_t tiles = 0;
+    BlockState* st = nullptr;
+    const unsigned long long* rp = nullptr;
+    const double* u1 = nullptr;
+    const double* u2 = nullptr;
+    const double2* T64 = nullptr;  // hoisted (x,y) (Gaussian) / (ln(-ln u), ln(-ln v)) (Gumbel fp64), or null
+    double* partials = nullptr;
+    unsigned* tickets = nullptr;
+};
+void run_variance(Ctx& c, const VarIO& v);
 
 void run_loglik(Ctx& c, int family, const double* d_theta, const double* u1, const double* u2,
                 const std::vector<uint64_t>& off, double* d_out);

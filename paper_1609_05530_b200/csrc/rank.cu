@@ -24,7 +24,11 @@
 // scratch). Each level shrinks an oversize range's key span by >= nb, so
 // the refinement terminates in a few levels even for adversarial inputs;
 // uniform-marginal data (every BASELINE config) finishes in level 0.
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.hpp"
@@ -277,7 +281,7 @@ __global__ void __launch_bounds__(RT) k_scatter(const RankRange* rr, int nr, con
 // by counting inside the bucket (L1-resident neighbours).
 __global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const unsigned long long* dkey,
                                             const uint32_t* didx, const uint32_t* hist, const uint32_t* bstart,
-                                            uint64_t n_rows, uint32_t* o_r2, uint32_t* o_pos, uint32_t* o_lt) {
+                                            uint64_t n_rows, unsigned long long* o_rp) {
     const int r = range_of_tile(rr, nr, blockIdx.x);
     const RankRange R = rr[r];
     const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
@@ -312,13 +316,12 @@ __global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const 
             pos = lt + before;
         }
         const uint64_t o = static_cast<uint64_t>(R.col) * n_rows + R.out_base + id;
-        o_r2[o] = 2u * lt + eq + 1u;
-        o_pos[o] = pos;
-        o_lt[o] = lt;
+        o_rp[o] = pack_rank(2u * lt + eq + 1u, pos);
     }
 }
 
-__global__ void k_ranks_to_u(const Seg* segs, int nseg, const uint32_t* r2, uint64_t n_rows, double* u1, double* u2) {
+__global__ void k_ranks_to_u(const Seg* segs, int nseg, const unsigned long long* rp, uint64_t n_rows, double* u1,
+                             double* u2) {
     const int m = seg_of_tile(segs, nseg, blockIdx.x);
     const Seg S = segs[m];
     const uint32_t begin = (blockIdx.x - S.tile0) * RTILE;
@@ -327,29 +330,354 @@ __global__ void k_ranks_to_u(const Seg* segs, int nseg, const uint32_t* r2, uint
     for (uint32_t i = begin + threadIdx.x; i < end; i += RT) {
         const uint64_t row = S.begin + i;
         // pseudo_obs.hpp:59-60: avg = 0.5*((i+1)+(j+1)); u = avg*scale
-        u1[row] = __dmul_rn(0.5 * static_cast<double>(r2[row]), scale);
-        u2[row] = __dmul_rn(0.5 * static_cast<double>(r2[n_rows + row]), scale);
+        u1[row] = __dmul_rn(0.5 * static_cast<double>(rank_r2(rp[row])), scale);
+        u2[row] = __dmul_rn(0.5 * static_cast<double>(rank_r2(rp[n_rows + row])), scale);
     }
 }
 
 uint32_t tiles_of(uint64_t n) { return static_cast<uint32_t>((n + RTILE - 1) / RTILE); }
 
+// ====================================================================
+// Cluster path: one thread-block cluster ranks one (column, segment) with
+// the whole segment held in the cluster's distributed shared memory.
+//   1. each CTA loads its slice of the column (HBM, once), cluster-wide
+//      min/max through DSMEM
+//   2. value-linear split of [min, max] into CL contiguous value ranges
+//      (one per CTA) x NBL local buckets; every CTA counts what it sends
+//      to each peer; the CL x CL count matrix is read through DSMEM
+//   3. every element is stored (key, row) into its value-range owner's
+//      receive buffer (DSMEM stores)
+//   4. each owner counting-sorts its elements into NBL local buckets and
+//      ranks every element by counting inside its bucket; lt = elements in
+//      lower value ranges + bucket start + #less
+// HBM traffic: 8 B read + 8 B (packed r2|pos) write per element. A slice
+// whose received count would overflow its buffer (heavily skewed data) or
+// a non-finite range falls back to the global path.
+constexpr int CT = 512;  // threads per cluster CTA
+constexpr int kMaxCluster = 16;
+constexpr size_t kSmemLimit = 227 * 1024 - 4096;  // leave room for static shared memory
+
+struct ClusterJob {
+    uint64_t begin;
+    uint32_t n, col, seg, pad;
+};
+
+struct ClusterPlan {
+    int cl = 0;            // CTAs per cluster (0: no cluster path)
+    uint32_t s = 0;        // max slice
+    uint32_t rcap = 0;     // receive capacity per CTA
+    uint32_t nbl = 0;      // local buckets per CTA
+    size_t smem = 0;
+};
+
+inline bool getenv_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && v[0] && v[0] != '0';
+}
+
+inline ClusterPlan plan_for(uint64_t nmax, int cl) {
+    ClusterPlan p;
+    p.cl = cl;
+    p.s = static_cast<uint32_t>((nmax + cl - 1) / cl);
+    const uint32_t slack = std::max<uint32_t>(256u, static_cast<uint32_t>(6.0 * std::sqrt(static_cast<double>(p.s))));
+    p.rcap = (p.s + slack + 31u) & ~31u;
+    p.nbl = std::max<uint32_t>(1u, p.s / 6);
+    p.smem = static_cast<size_t>(p.rcap) * 14 + static_cast<size_t>(p.nbl) * 8 + 64;
+    return p;
+}
+
+inline ClusterPlan plan_cluster(uint64_t nmax) {
+    int forced = 0;
+    if (const char* v = std::getenv("PCB_RANK_CL")) forced = std::atoi(v);
+    for (int cl = 1; cl <= kMaxCluster; ++cl) {
+        if (forced && cl != forced) continue;
+        ClusterPlan p = plan_for(nmax, cl);
+        if (p.rcap < 65535 && p.smem <= kSmemLimit) return p;
+    }
+    return ClusterPlan{};
+}
+
+__device__ __forceinline__ uint32_t agg_add(uint32_t* base, uint32_t key, bool valid) {
+    const unsigned active = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return 0u;
+    const unsigned peers = __match_any_sync(active, key);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    uint32_t b = 0;
+    if (lane == leader) b = atomicAdd(base + key, static_cast<uint32_t>(__popc(peers)));
+    b = __shfl_sync(peers, b, leader);
+    return b + static_cast<uint32_t>(__popc(peers & ((1u << lane) - 1u)));
+}
+
+__global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, const double* c0, const double* c1,
+                                                       uint64_t n_rows, unsigned long long* rp, int32_t* fb,
+                                                       int32_t* bad, int CL, uint32_t RCAP, uint32_t NBL) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int r = static_cast<int>(cluster.block_rank());
+    const uint32_t jid = blockIdx.x / CL;
+    const ClusterJob J = jobs[jid];
+    const double* x = (J.col ? c1 : c0) + J.begin;
+    const uint32_t S = (J.n + CL - 1) / CL;
+    const uint32_t a = min(J.n, r * S), e = min(J.n, a + S);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long* recv_key = reinterpret_cast<unsigned long long*>(smem);
+    uint32_t* recv_idx = reinterpret_cast<uint32_t*>(recv_key + RCAP);
+    uint32_t* lh_cnt = recv_idx + RCAP;
+    uint32_t* lh_start = lh_cnt + NBL;
+    uint16_t* perm = reinterpret_cast<uint16_t*>(lh_start + NBL);
+
+    __shared__ unsigned long long s_kmin[CT / 32], s_kmax[CT / 32];
+    __shared__ unsigned long long s_rmin, s_rmax;  // this CTA's reduced extremes (read remotely)
+    __shared__ int s_bad;
+    __shared__ uint32_t s_cnt[kMaxCluster];   // elements this CTA sends to each peer (read remotely)
+    __shared__ uint32_t s_cur[kMaxCluster];   // send cursors
+    __shared__ uint32_t s_mat[kMaxCluster * kMaxCluster];
+    __shared__ uint32_t s_warp[CT / 32];
+
+    // ---- 1. slice extremes
+    unsigned long long kmn = ~0ull, kmx = 0ull;
+    bool fin = true;
+    for (uint32_t i = a + tid; i < e; i += CT) {
+        const double v = x[i];
+        fin &= isfinite(v);
+        const unsigned long long k = order_key(v);
+        kmn = min(kmn, k);
+        kmx = max(kmx, k);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+        kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+    }
+    fin = __all_sync(0xffffffffu, fin);
+    if (tid == 0) s_bad = 0;
+    if (tid < kMaxCluster) s_cnt[tid] = 0u;
+    __syncthreads();
+    if (lane == 0) {
+        s_kmin[wid] = kmn;
+        s_kmax[wid] = kmx;
+        if (!fin) s_bad = 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < CT / 32; ++w) {
+            kmn = min(kmn, s_kmin[w]);
+            kmx = max(kmx, s_kmax[w]);
+        }
+        s_rmin = kmn;
+        s_rmax = kmx;
+    }
+    cluster.sync();
+    __shared__ unsigned long long s_gmin, s_gmax;
+    __shared__ int s_gbad;
+    if (tid == 0) {
+        unsigned long long gmn = ~0ull, gmx = 0ull;
+        int gb = 0;
+        for (int q = 0; q < CL; ++q) {
+            gmn = min(gmn, *cluster.map_shared_rank(&s_rmin, q));
+            gmx = max(gmx, *cluster.map_shared_rank(&s_rmax, q));
+            gb |= *cluster.map_shared_rank(&s_bad, q);
+        }
+        s_gmin = gmn;
+        s_gmax = gmx;
+        s_gbad = gb;
+    }
+    __syncthreads();
+    const unsigned long long gmin = s_gmin, gmax = s_gmax;
+    const double vmin = key_value(gmin), vmax = key_value(gmax);
+    const double hm = 0.5 * vmin;
+    const double nbt = static_cast<double>(CL) * static_cast<double>(NBL);
+    const double scale = nbt / (0.5 * vmax - hm);
+    const bool constant = gmin == gmax;
+    if (s_gbad || constant || !(isfinite(scale) && scale > 0.0 && isfinite(hm))) {
+        if (s_gbad) {
+            if (r == 0 && tid == 0) bad[J.seg] = 1;
+        } else if (constant) {  // one tie run: avg rank (n+1)/2 for all, stable positions = row order
+            for (uint32_t i = a + tid; i < e; i += CT)
+                rp[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = pack_rank(J.n + 1u, i);
+        } else if (r == 0 && tid == 0) {
+            fb[jid] = 1;
+        }
+        cluster.sync();  // peers may still be reading this CTA's shared memory
+        return;
+    }
+    const uint32_t nbtot = static_cast<uint32_t>(CL) * NBL;
+    auto bucket = [&](unsigned long long k) -> uint32_t {
+        const double t = (0.5 * key_value(k) - hm) * scale;
+        return t < static_cast<double>(nbtot) ? static_cast<uint32_t>(t) : nbtot - 1u;
+    };
+
+    // ---- 2. counts to each value-range owner
+    const uint32_t iters = (e - a + CT - 1) / CT;
+    for (uint32_t it = 0; it < iters; ++it) {
+        const uint32_t i = a + it * CT + tid;
+        const bool valid = i < e;
+        uint32_t d = 0;
+        if (valid) d = bucket(order_key(x[i])) / NBL;
+        agg_add(s_cnt, d, valid);
+    }
+    cluster.sync();
+    if (tid < CL * CL) s_mat[tid] = *cluster.map_shared_rank(&s_cnt[tid % CL], tid / CL);  // [src][dst]
+    __syncthreads();
+    __shared__ uint32_t s_total, s_base;
+    __shared__ int s_over;
+    if (tid == 0) {
+        int over = 0;
+        uint32_t base = 0, total = 0;
+        for (int d = 0; d < CL; ++d) {
+            uint32_t col = 0;
+            for (int q = 0; q < CL; ++q) col += s_mat[q * CL + d];
+            if (col > RCAP) over = 1;
+            if (d < r) base += col;
+            if (d == r) total = col;
+        }
+        for (int d = 0; d < CL; ++d) {
+            uint32_t o = 0;
+            for (int q = 0; q < r; ++q) o += s_mat[q * CL + d];
+            s_cur[d] = o;
+        }
+        s_total = total;
+        s_base = base;
+        s_over = over;
+    }
+    __syncthreads();
+    if (s_over) {
+        if (r == 0 && tid == 0) fb[jid] = 1;
+        cluster.sync();
+        return;
+    }
+
+    // ---- 3. scatter (key, row) to the owners (DSMEM stores)
+    for (uint32_t it = 0; it < iters; ++it) {
+        const uint32_t i = a + it * CT + tid;
+        const bool valid = i < e;
+        unsigned long long k = 0;
+        uint32_t d = 0;
+        if (valid) {
+            k = order_key(x[i]);
+            d = bucket(k) / NBL;
+        }
+        const uint32_t slot = agg_add(s_cur, d, valid);
+        if (valid) {
+            *cluster.map_shared_rank(recv_key + slot, d) = k;
+            *cluster.map_shared_rank(recv_idx + slot, d) = i;
+        }
+    }
+    cluster.sync();  // all stores into every receive buffer are visible; no remote access after this
+
+    // ---- 4. local counting sort into NBL buckets
+    const uint32_t T = s_total, base = s_base;
+    const uint32_t b0 = static_cast<uint32_t>(r) * NBL;
+    for (uint32_t q = tid; q < NBL; q += CT) lh_cnt[q] = 0u;
+    __syncthreads();
+    for (uint32_t j = tid; j < T; j += CT) atomicAdd(lh_cnt + (bucket(recv_key[j]) - b0), 1u);
+    __syncthreads();
+    // exclusive scan lh_cnt -> lh_start (block scan in chunks of CT)
+    __shared__ uint32_t s_carry;
+    if (tid == 0) s_carry = 0u;
+    __syncthreads();
+    for (uint32_t q0 = 0; q0 < NBL; q0 += CT) {
+        const uint32_t q = q0 + tid;
+        const uint32_t v = q < NBL ? lh_cnt[q] : 0u;
+        uint32_t x2 = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x2, o);
+            if (lane >= o) x2 += y;
+        }
+        if (lane == 31) s_warp[wid] = x2;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t z = lane < CT / 32 ? s_warp[lane] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+                if (lane >= o) z += y;
+            }
+            if (lane < CT / 32) s_warp[lane] = z;
+        }
+        __syncthreads();
+        const uint32_t excl = s_carry + (wid ? s_warp[wid - 1] : 0u) + x2 - v;
+        if (q < NBL) {
+            lh_start[q] = excl;
+            lh_cnt[q] = excl;  // cursor
+        }
+        __syncthreads();
+        if (tid == CT - 1) s_carry = excl + v;
+        __syncthreads();
+    }
+    for (uint32_t j = tid; j < T; j += CT) {
+        const uint32_t slot = atomicAdd(lh_cnt + (bucket(recv_key[j]) - b0), 1u);
+        perm[slot] = static_cast<uint16_t>(j);
+    }
+    __syncthreads();
+
+    // ---- 5. rank inside each bucket; write packed (r2 | pos)
+    unsigned long long* out = rp + static_cast<uint64_t>(J.col) * n_rows + J.begin;
+    for (uint32_t j = tid; j < T; j += CT) {
+        const unsigned long long k = recv_key[j];
+        const uint32_t id = recv_idx[j];
+        const uint32_t lb = bucket(k) - b0;
+        const uint32_t s0 = lh_start[lb];
+        const uint32_t s1 = lb + 1 < NBL ? lh_start[lb + 1] : T;
+        uint32_t less = 0, same = 0, before = 0;
+        for (uint32_t q = s0; q < s1; ++q) {
+            const uint32_t o = perm[q];
+            const unsigned long long kq = recv_key[o];
+            less += kq < k;
+            const bool eqk = kq == k;
+            same += eqk;
+            before += eqk && recv_idx[o] < id;
+        }
+        const uint32_t lt = base + s0 + less;
+        out[id] = pack_rank(2u * lt + same + 1u, lt + before);
+    }
+}
+
+void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, uint32_t njobs, const double* c0,
+                         const double* c1, uint64_t n_rows, unsigned long long* rp, int32_t* fb, int32_t* bad) {
+    PCB_CUDA(cudaFuncSetAttribute(k_rank_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(p.smem)));
+    if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(k_rank_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(njobs * static_cast<uint32_t>(p.cl));
+    cfg.blockDim = dim3(CT);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(p.cl);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, rp, fb, bad, p.cl, p.rcap, p.nbl));
+    c.count_launch();
+}
+
 }  // namespace
 
-void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_rows, const std::vector<uint64_t>& off,
-               RankOut out, int32_t* d_bad) {
+namespace {
+
+// Global-memory multi-level path for the (column, segment) jobs in `jobs`
+// (encoded col * K + m): segments too large for one cluster, or whose values
+// are too skewed for the cluster's value-linear split.
+void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_rows,
+                      const std::vector<uint64_t>& off, const std::vector<uint32_t>& jobs, RankOut out,
+                      int32_t* d_bad) {
     const size_t K = off.size() - 1;
-    if (K == 0 || n_rows == 0) return;
-    for (size_t m = 0; m < K; ++m)
-        if (off[m + 1] - off[m] >= (1ull << 30)) throw Error(2, "segment too large for 32-bit ranks");
     cudaStream_t st = c.stream;
-    // ---- level 0: one range per (column, segment)
+    // ---- level 0: one range per (column, segment) job
     std::vector<RankRange> ranges;
-    ranges.reserve(2 * K);
+    ranges.reserve(jobs.size());
     uint64_t bsum = 0;
     uint32_t tiles = 0;
-    for (int col = 0; col < 2; ++col)
-        for (size_t m = 0; m < K; ++m) {
+    for (uint32_t job : jobs) {
+            const int col = static_cast<int>(job / K);
+            const size_t m = job % K;
             RankRange R;
             std::memset(&R, 0, sizeof R);
             const uint64_t n = off[m + 1] - off[m];
@@ -370,7 +698,8 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
             bsum += R.nb;
             tiles += tiles_of(n);
             ranges.push_back(R);
-        }
+    }
+    if (ranges.empty()) return;
     const uint64_t total = 2 * n_rows;
     auto* keyA = c.ws.get_t<unsigned long long>("rank.keyA", total);
     auto* idxA = c.ws.get_t<uint32_t>("rank.idxA", total);
@@ -397,7 +726,7 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
         k_scan<<<nr, 1024, 0, st>>>(d_rr, hist, bstart, cursor, ov, ovn, ov_cap);
         if (l0) k_scatter<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
         else k_scatter<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
-        k_rank<<<ntiles, RT, 0, st>>>(d_rr, nr, dkey, didx, hist, bstart, n_rows, out.r2, out.pos, out.lt);
+        k_rank<<<ntiles, RT, 0, st>>>(d_rr, nr, dkey, didx, hist, bstart, n_rows, out.rp);
         c.count_launch(6);
         PCB_CUDA(cudaMemcpyAsync(h_ovn, ovn, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         PCB_CUDA(cudaStreamSynchronize(st));
@@ -460,7 +789,45 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
     }
 }
 
-void ranks_to_u(Ctx& c, const uint32_t* r2, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
+}  // namespace
+
+void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_rows, const std::vector<uint64_t>& off,
+               RankOut out, int32_t* d_bad) {
+    const size_t K = off.size() - 1;
+    if (K == 0 || n_rows == 0) return;
+    uint64_t nmax = 0;
+    for (size_t m = 0; m < K; ++m) {
+        const uint64_t n = off[m + 1] - off[m];
+        if (n >= (1ull << 30)) throw Error(2, "segment too large for 32-bit ranks");
+        nmax = std::max(nmax, n);
+    }
+    std::vector<uint32_t> fallback;
+    ClusterPlan plan = plan_cluster(nmax);
+    if (plan.cl > 0 && !getenv_flag("PCB_RANK_GLOBAL")) {
+        const uint32_t njobs = static_cast<uint32_t>(2 * K);
+        auto* jobs = c.ws.get_t<ClusterJob>("rank.cjobs", njobs);
+        auto* fb = c.ws.get_t<int32_t>("rank.cfb", njobs);
+        std::vector<ClusterJob> hj(njobs);
+        for (uint32_t j = 0; j < njobs; ++j) {
+            const size_t m = j % K;
+            hj[j] = ClusterJob{off[m], static_cast<uint32_t>(off[m + 1] - off[m]), static_cast<uint32_t>(j / K),
+                               static_cast<uint32_t>(m), 0u};
+        }
+        PCB_CUDA(cudaMemcpyAsync(jobs, hj.data(), njobs * sizeof(ClusterJob), cudaMemcpyHostToDevice, c.stream));
+        PCB_CUDA(cudaMemsetAsync(fb, 0, njobs * sizeof(int32_t), c.stream));
+        launch_rank_cluster(c, plan, jobs, njobs, d_col1, d_col2, n_rows, out.rp, fb, d_bad);
+        std::vector<int32_t> hfb(njobs);
+        PCB_CUDA(cudaMemcpyAsync(hfb.data(), fb, njobs * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+        for (uint32_t j = 0; j < njobs; ++j)
+            if (hfb[j]) fallback.push_back(j);
+    } else {
+        for (uint32_t j = 0; j < 2 * K; ++j) fallback.push_back(j);
+    }
+    run_ranks_global(c, d_col1, d_col2, n_rows, off, fallback, out, d_bad);
+}
+
+void ranks_to_u(Ctx& c, const unsigned long long* rp, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
                 double* u2) {
     const size_t K = off.size() - 1;
     std::vector<Seg> segs(K);
@@ -472,7 +839,7 @@ void ranks_to_u(Ctx& c, const uint32_t* r2, uint64_t n_rows, const std::vector<u
     if (tiles == 0) return;
     auto* d_segs = c.ws.get_t<Seg>("u.segs", K);
     PCB_CUDA(cudaMemcpyAsync(d_segs, segs.data(), K * sizeof(Seg), cudaMemcpyHostToDevice, c.stream));
-    k_ranks_to_u<<<tiles, RT, 0, c.stream>>>(d_segs, static_cast<int>(K), r2, n_rows, u1, u2);
+    k_ranks_to_u<<<tiles, RT, 0, c.stream>>>(d_segs, static_cast<int>(K), rp, n_rows, u1, u2);
     c.count_launch();
 }
 

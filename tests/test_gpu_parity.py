@@ -262,3 +262,53 @@ def test_c1_golden_fixture(ctx):
     U = pcb.normalized_ranks(X, pcb.partition(10000, 10).offsets, ctx=ctx)
     import hashlib
     assert hashlib.sha256(U.u1.tobytes() + U.u2.tobytes()).hexdigest() == meta["ranks_sha256"]
+
+
+# ------------------------------------------- cluster vs global code paths
+@pytest.fixture
+def env(monkeypatch):
+    return monkeypatch
+
+
+@pytest.mark.parametrize("n,k", [(300000, 1), (250000, 2), (125000, 1)])
+def test_rank_large_and_cluster_segments(ctx, orc, n, k):
+    rng = np.random.default_rng(n + 7)
+    c1 = rng.uniform(size=n)
+    c2 = np.round(rng.standard_normal(n), 2)  # heavy ties spanning cluster slices
+    off = np.linspace(0, n, k + 1).astype(np.uint64)
+    U = pcb.normalized_ranks(pcb.DataMatrix(c1, c2), off, ctx=ctx)
+    assert np.array_equal(U.u1, oracle_ranks(orc, c1, off))
+    assert np.array_equal(U.u2, oracle_ranks(orc, c2, off))
+
+
+def test_rank_forced_global_path_identical(ctx, env):
+    rng = np.random.default_rng(5)
+    n = 100000
+    X = pcb.DataMatrix(rng.uniform(size=n), np.round(rng.uniform(size=n), 3))
+    off = np.linspace(0, n, 5).astype(np.uint64)
+    a = pcb.normalized_ranks(X, off, ctx=ctx)
+    env.setenv("PCB_RANK_GLOBAL", "1")
+    b = pcb.normalized_ranks(X, off, ctx=ctx)
+    assert np.array_equal(a.u1, b.u1) and np.array_equal(a.u2, b.u2)
+
+
+@pytest.mark.parametrize("fam,theta", FAMS)
+def test_variance_cluster_vs_global(ctx, orc, env, fam, theta):
+    n, k = 60000, 3
+    X = pcb.sample_matrix(fam, theta, n, k, ctx=ctx)
+    X = pcb.DataMatrix(X.col1, np.round(X.col2, 4))  # ties in column 2
+    off = orc.partition(n, k)
+    a = pcb.fit_blocks(fam, X, off, ctx=ctx)
+    env.setenv("PCB_VAR_GLOBAL", "1")
+    b = pcb.fit_blocks(fam, X, off, ctx=ctx)
+    want = orc.fit_blocks(fam, X.col1, X.col2, off)
+    check_records(a, want, TOL64)
+    check_records(b, want, TOL64)
+
+
+def test_variance_large_segment_global(ctx, orc):
+    n = 320000
+    X = pcb.sample_matrix(2, 3.0, n, 1, ctx=ctx)
+    got = pcb.fit_blocks(2, X, [0, n], ctx=ctx)
+    want = orc.fit_blocks(2, X.col1, X.col2, [0, n])
+    check_records(got, want, TOL64)
