@@ -152,7 +152,7 @@ void finish_stage_times(pcb::Ctx& c) {
         }
         c.stage_ms[k] = ms;
     }
-    c.n_stage = 7;
+    c.n_stage = 9;
 }
 
 // raw columns (device) -> ranks -> fit -> variance; records to d_out (device)

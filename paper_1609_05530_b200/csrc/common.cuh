@@ -93,7 +93,7 @@ __device__ __forceinline__ double key_value(uint64_t k) {
 // Fit / variance kernels map one CTA to one tile of FTILE points that never
 // straddles a segment (Seg::tile0 = first tile of the segment).
 constexpr int FT = 256;  // threads per tile CTA
-constexpr int PPT = 8;   // points per thread per tile
+constexpr int PPT = 32;  // points per thread per tile
 constexpr uint32_t FTILE = FT * PPT;
 
 // Stores this tile's NV partial sums; the segment's last-arriving tile sums
@@ -130,11 +130,18 @@ __device__ bool tile_reduce(double (&v)[NV], double* sh, double* partials, unsig
     return true;
 }
 
-__host__ __device__ __forceinline__ unsigned long long pack_rank(uint32_t r2, uint32_t pos) {
-    return static_cast<unsigned long long>(r2) | (static_cast<unsigned long long>(pos) << 32);
+// Packed rank of one element of one column (see internal.hpp RankOut):
+// bits 0-31 r2, bits 32-62 stable sorted position, bit 63 = first position of
+// its tie run (pos == run start; every element of an untied value has it).
+__host__ __device__ __forceinline__ unsigned long long pack_rank(uint32_t r2, uint32_t pos, bool first) {
+    return static_cast<unsigned long long>(r2) | (static_cast<unsigned long long>(pos & 0x7fffffffu) << 32) |
+           (first ? 0x8000000000000000ull : 0ull);
 }
 __host__ __device__ __forceinline__ uint32_t rank_r2(unsigned long long rp) { return static_cast<uint32_t>(rp); }
-__host__ __device__ __forceinline__ uint32_t rank_pos(unsigned long long rp) { return static_cast<uint32_t>(rp >> 32); }
+__host__ __device__ __forceinline__ uint32_t rank_pos(unsigned long long rp) {
+    return static_cast<uint32_t>(rp >> 32) & 0x7fffffffu;
+}
+__host__ __device__ __forceinline__ bool rank_first(unsigned long long rp) { return (rp >> 63) != 0; }
 
 // (u, v) of a point: the caller's pseudo-observations, or exactly
 // normalized_rank_column's value from the packed rank (pseudo_obs.hpp:59-60).

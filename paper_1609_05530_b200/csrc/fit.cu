@@ -17,6 +17,7 @@
 // atomics, so results do not depend on scheduling, the GPU count or the run.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -26,9 +27,17 @@
 namespace pcb {
 namespace {
 
+bool getenv_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && v[0] && v[0] != '0';
+}
+
 constexpr int kMaxPasses = 64;
-constexpr double kTol64 = 2e-8;  // Newton step tolerance (relative); error after ~C*tol^2
+// Newton step tolerances (relative to max(1,|theta|)). A converged step of
+// size d leaves an error ~C*d^2 (quadratic convergence): 1e-6 -> ~1e-12.
+constexpr double kTol64 = 1e-6;
 constexpr double kTol32 = 1e-6;
+constexpr int kWarmPasses = 2;  // fp32 warm-up passes before the fp64 passes (fp64 mode)
 
 // Spearman-rho -> theta inversion tables for the Archimedean init.
 constexpr int NTAB = 256;
@@ -53,6 +62,14 @@ __device__ double invert_table(const double* rho, const double* th, double r) {
 // the domain). Runs in one thread per block.
 __device__ void newton_update(BlockState& s, int fam, double S, double H, double tol, unsigned* running) {
     s.iters += 1;
+    if (tol < 0.0) {  // warm-up pass (fp32 per-point arithmetic): move theta, decide nothing
+        if (isfinite(S) && isfinite(H) && H < 0.0) {
+            double cand = s.theta - S / H;
+            if (fam == kGumbel) cand = fmax(cand, 1.0);
+            if (isfinite(cand) && !(fam == kFrank && fabs(cand) < 1e-6)) s.theta = cand;
+        }
+        return;
+    }
     s.S = S;
     s.H = H;
     double t = s.theta;
@@ -150,7 +167,8 @@ __global__ void k_init_state(BlockState* st, const Seg* segs, int nseg, const in
 template <int FAM, class TO>
 __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs, int nseg,
                                                const unsigned long long* rp, const double* u1, const double* u2,
-                                               uint64_t n_rows, TO* T, double* partials, unsigned* tickets,
+                                               uint64_t n_rows, TO* T, float2* T32, const double* gtab,
+                                               const uint64_t* goff, double* partials, unsigned* tickets,
                                                unsigned* running, int with_fit) {
     const uint32_t tile = blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
@@ -170,10 +188,18 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
         u = clamp_unit(u);
         w = clamp_unit(w);
         if (FAM == kGaussian) {
-            const double x = dev_phi_inv(u), y = dev_phi_inv(w);
+            double x, y;
+            if (gtab) {  // Phi^-1 depends only on the rank: per-block-size table (bit-identical values)
+                const double* tb = gtab + goff[m];
+                x = tb[rank_r2(rp[row])];
+                y = tb[rank_r2(rp[n_rows + row])];
+            } else {
+                x = dev_phi_inv(u);
+                y = dev_phi_inv(w);
+                T[row] = TO{static_cast<decltype(TO::x)>(x), static_cast<decltype(TO::x)>(y)};
+            }
             v[0] += x * y;
             v[1] += x * x + y * y;
-            T[row] = TO{static_cast<decltype(TO::x)>(x), static_cast<decltype(TO::x)>(y)};
         } else {
             v[0] += u * w;
             if (FAM == kFrank) {
@@ -181,9 +207,11 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
                     T[row] = TO{static_cast<decltype(TO::x)>(frank_edge(u)), static_cast<decltype(TO::x)>(frank_edge(w))};
                 else
                     T[row] = TO{static_cast<decltype(TO::x)>(u), static_cast<decltype(TO::x)>(w)};
+                if (T32) T32[row] = float2{frank_edge(u), frank_edge(w)};
             } else {
                 const double lx = log(-log(u)), ly = log(-log(w));
                 T[row] = TO{static_cast<decltype(TO::x)>(lx), static_cast<decltype(TO::x)>(ly)};
+                if (T32) T32[row] = float2{static_cast<float>(lx), static_cast<float>(ly)};
             }
         }
     }
@@ -252,7 +280,7 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
 // current theta, deterministic block reduction, in-kernel Newton update.
 template <int FAM, class TI>
 __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int nseg, const TI* __restrict__ T,
-                                           double* partials, unsigned* tickets, unsigned* running) {
+                                           double* partials, unsigned* tickets, unsigned* running, double tol) {
     const uint32_t tile = blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
@@ -340,9 +368,17 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
     if (!tile_reduce<2>(v, sh, partials, tickets, S, m, tile)) return;
     if (threadIdx.x == 0) {
         BlockState s = st[m];
-        newton_update(s, FAM, v[0], v[1], sizeof(TI) == 16 ? kTol64 : kTol32, running);
+        newton_update(s, FAM, v[0], v[1], tol, running);
         st[m] = s;
     }
+}
+
+// Phi^-1((0.5*r2)/(n+1)) for every r2 in [2, 2n]: the Gaussian scores of a
+// block of n ranked rows (same arithmetic as the per-point path).
+__global__ void k_gauss_table(double* tab, uint32_t n) {
+    const double scale = 1.0 / (static_cast<double>(n) + 1.0);
+    for (uint32_t r2 = blockIdx.x * blockDim.x + threadIdx.x; r2 <= 2 * n; r2 += gridDim.x * blockDim.x)
+        tab[r2] = r2 >= 2 ? dev_phi_inv(clamp_unit(__dmul_rn(0.5 * static_cast<double>(r2), scale))) : 0.0;
 }
 
 struct RecordOut {  // == pcb_fit_result
@@ -448,25 +484,28 @@ uint32_t ftiles(uint64_t n) { return static_cast<uint32_t>((n + FTILE - 1) / FTI
 
 template <int FAM>
 void launch_prepare(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, const FitIO& io, void* T,
-                    bool fp32T, double* part, unsigned* tick, unsigned* running, int with_fit) {
+                    bool fp32T, float2* T32, const double* gtab, const uint64_t* goff, double* part, unsigned* tick,
+                    unsigned* running, int with_fit) {
     if (fp32T)
         k_prepare<FAM, float2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.rp, io.u1, io.u2, io.n_rows,
-                                                          static_cast<float2*>(T), part, tick, running, with_fit);
+                                                          static_cast<float2*>(T), nullptr, gtab, goff, part, tick,
+                                                          running, with_fit);
     else
         k_prepare<FAM, double2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.rp, io.u1, io.u2, io.n_rows,
-                                                           static_cast<double2*>(T), part, tick, running, with_fit);
+                                                           static_cast<double2*>(T), T32, gtab, goff, part, tick,
+                                                           running, with_fit);
     c.count_launch();
 }
 
 template <int FAM>
-void launch_lik(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, int prec, const void* T, double* part,
-                unsigned* tick, unsigned* running) {
-    if (prec == 1)
+void launch_lik(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, bool f32, const void* T,
+                double* part, unsigned* tick, unsigned* running, double tol) {
+    if (f32)
         k_lik<FAM, float2><<<tiles, FT, 0, c.stream>>>(st, segs, K, static_cast<const float2*>(T), part, tick,
-                                                       running);
+                                                       running, tol);
     else
         k_lik<FAM, double2><<<tiles, FT, 0, c.stream>>>(st, segs, K, static_cast<const double2*>(T), part, tick,
-                                                        running);
+                                                        running, tol);
     c.count_launch();
 }
 
@@ -514,34 +553,81 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
     // T: fp32 only for the Archimedean fp32 likelihood path; the Gaussian
     // (x, y) pair is always fp64 (it only feeds the variance pass).
     const bool fp32T = io.precision == 1 && fam != kGaussian;
-    void* T = c.ws.get("fit.T", io.n_rows * (fp32T ? sizeof(float2) : sizeof(double2)));
+    // fp64 mode: fp32 warm-up passes from a float copy of T, then fp64 passes
+    // decide convergence (the answer is the fp64 score root either way)
+    const bool warm = io.precision == 0 && fam != kGaussian && io.do_fit && !getenv_flag("PCB_NO_WARM32");
+    // Gaussian scores by rank table (rank-derived u only; few distinct block sizes)
+    const double* gtab = nullptr;
+    const uint64_t* goff = nullptr;
+    if (fam == kGaussian && !io.u1 && !getenv_flag("PCB_NO_GTAB")) {
+        std::vector<uint32_t> sizes;
+        for (int m = 0; m < K; ++m)
+            if (std::find(sizes.begin(), sizes.end(), segs[m].n) == sizes.end()) sizes.push_back(segs[m].n);
+        if (sizes.size() <= 16) {
+            std::vector<uint64_t> base(sizes.size());
+            uint64_t tot = 0;
+            for (size_t q = 0; q < sizes.size(); ++q) {
+                base[q] = tot;
+                tot += 2ull * sizes[q] + 1;
+            }
+            auto* tab = c.ws.get_t<double>("fit.gtab", tot);
+            std::vector<uint64_t> hoff(K);
+            for (int m = 0; m < K; ++m)
+                hoff[m] = base[std::find(sizes.begin(), sizes.end(), segs[m].n) - sizes.begin()];
+            auto* d_off = c.ws.get_t<uint64_t>("fit.goff", K);
+            PCB_CUDA(cudaMemcpyAsync(d_off, hoff.data(), K * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+            for (size_t q = 0; q < sizes.size(); ++q) {
+                const uint32_t nn = sizes[q];
+                k_gauss_table<<<std::min<uint32_t>(148u * 8u, (2 * nn + 256) / 256), 256, 0, s>>>(tab + base[q], nn);
+                c.count_launch();
+            }
+            gtab = tab;
+            goff = d_off;
+        }
+    }
+    void* T = gtab ? nullptr : c.ws.get("fit.T", io.n_rows * (fp32T ? sizeof(float2) : sizeof(double2)));
+    float2* T32 = warm ? c.ws.get_t<float2>("fit.T32", io.n_rows) : nullptr;
     if (tiles > 0) {
         const int with_fit = io.do_fit ? 1 : 0;
-        if (fam == kGaussian) launch_prepare<kGaussian>(c, tiles, st, d_segs, K, io, T, fp32T, part, tick, running, with_fit);
-        else if (fam == kFrank) launch_prepare<kFrank>(c, tiles, st, d_segs, K, io, T, fp32T, part, tick, running, with_fit);
-        else launch_prepare<kGumbel>(c, tiles, st, d_segs, K, io, T, fp32T, part, tick, running, with_fit);
+        if (fam == kGaussian)
+            launch_prepare<kGaussian>(c, tiles, st, d_segs, K, io, T, fp32T, T32, gtab, goff, part, tick, running, with_fit);
+        else if (fam == kFrank)
+            launch_prepare<kFrank>(c, tiles, st, d_segs, K, io, T, fp32T, T32, gtab, goff, part, tick, running, with_fit);
+        else
+            launch_prepare<kGumbel>(c, tiles, st, d_segs, K, io, T, fp32T, T32, gtab, goff, part, tick, running, with_fit);
     }
     PCB_CUDA(cudaEventRecord(ev[2], s));
-    float lik_ms = 0.0f;
-    int lik_launches = 0;
+    float lik_ms = 0.0f, warm_ms = 0.0f;
+    int lik_launches = 0, warm_launches = 0;
     if (io.do_fit && fam != kGaussian && tiles > 0) {
         for (int pass = 0; pass < kMaxPasses; ++pass) {
+            const bool wp = warm && pass < kWarmPasses;
+            const bool f32 = wp || fp32T;
+            const void* Tp = wp ? static_cast<const void*>(T32) : T;
+            const double tol = wp ? -1.0 : (fp32T ? kTol32 : kTol64);
             PCB_CUDA(cudaEventRecord(ev[6], s));
-            if (fam == kFrank) launch_lik<kFrank>(c, tiles, st, d_segs, K, io.precision, T, part, tick, running);
-            else launch_lik<kGumbel>(c, tiles, st, d_segs, K, io.precision, T, part, tick, running);
+            if (fam == kFrank) launch_lik<kFrank>(c, tiles, st, d_segs, K, f32, Tp, part, tick, running, tol);
+            else launch_lik<kGumbel>(c, tiles, st, d_segs, K, f32, Tp, part, tick, running, tol);
             PCB_CUDA(cudaEventRecord(ev[7], s));
             PCB_CUDA(cudaMemcpyAsync(h_running, running, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
             PCB_CUDA(cudaStreamSynchronize(s));
             float ms = 0.0f;
             PCB_CUDA(cudaEventElapsedTime(&ms, ev[6], ev[7]));
-            lik_ms += ms;
-            ++lik_launches;
+            if (wp) {
+                warm_ms += ms;
+                ++warm_launches;
+            } else {
+                lik_ms += ms;
+                ++lik_launches;
+            }
             if (*h_running == 0) break;
         }
     }
     PCB_CUDA(cudaEventRecord(ev[3], s));
     c.stage_ms[5] = lik_ms;
     c.stage_ms[6] = lik_launches;
+    c.stage_ms[7] = warm_ms;
+    c.stage_ms[8] = warm_launches;
     if (io.do_variance && tiles > 0) {
         VarIO v;
         v.family = fam;
@@ -554,7 +640,9 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
         v.rp = io.rp;
         v.u1 = io.u1;
         v.u2 = io.u2;
-        v.T64 = (fam == kGaussian || (fam == kGumbel && !fp32T)) ? static_cast<const double2*>(T) : nullptr;
+        v.T64 = ((fam == kGaussian && !gtab) || (fam == kGumbel && !fp32T)) ? static_cast<const double2*>(T) : nullptr;
+        v.gtab = gtab;
+        v.goff = goff;
         v.partials = part;
         v.tickets = tick;
         run_variance(c, v);

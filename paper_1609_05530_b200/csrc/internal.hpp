@@ -65,7 +65,7 @@ struct Ctx {
     std::string err;
     Workspace ws;
     uint64_t launches = 0;
-    double stage_ms[8] = {0};
+    double stage_ms[12] = {0};
     int n_stage = 0;
     cudaEvent_t ev[8] = {};
     // pinned host staging for small results
@@ -89,9 +89,11 @@ struct Ctx {
 // ---------------------------------------------------------------- ranks
 // Segment-local bit-exact rank outputs, [2][n_rows] packed u64
 // (pack_rank in common.cuh):
-//   low 32  r2  = (i+1)+(j+1), twice the 1-based average rank of the tie run i..j
-//   high 32 pos = unique stable sorted position (ties ordered by row index)
-// A tie run is the set of sorted positions sharing one r2.
+//   bits 0-31  r2  = (i+1)+(j+1), twice the 1-based average rank of the tie run i..j
+//   bits 32-62 pos = unique stable sorted position (ties ordered by row index)
+//   bit  63    pos is the first position of its tie run
+// The run-start bits of a segment, set at the positions, mark where every
+// tie run begins; the variance finds a run's first position from them.
 struct RankOut {
     unsigned long long* rp;
 };
@@ -139,6 +141,8 @@ struct VarIO {
     const double* u1 = nullptr;
     const double* u2 = nullptr;
     const double2* T64 = nullptr;  // hoisted (x,y) (Gaussian) / (ln(-ln u), ln(-ln v)) (Gumbel fp64), or null
+    const double* gtab = nullptr;  // Gaussian scores by rank (fit.cu k_gauss_table), or null
+    const uint64_t* goff = nullptr;
     double* partials = nullptr;
     unsigned* tickets = nullptr;
 };

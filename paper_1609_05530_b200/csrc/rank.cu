@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "internal.hpp"
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const 
             pos = lt + before;
         }
         const uint64_t o = static_cast<uint64_t>(R.col) * n_rows + R.out_base + id;
-        o_rp[o] = pack_rank(2u * lt + eq + 1u, pos);
+        o_rp[o] = pack_rank(2u * lt + eq + 1u, pos, R.mode == 2 ? pos == R.run_start : pos == lt);
     }
 }
 
@@ -353,9 +354,13 @@ uint32_t tiles_of(uint64_t n) { return static_cast<uint32_t>((n + RTILE - 1) / R
 // HBM traffic: 8 B read + 8 B (packed r2|pos) write per element. A slice
 // whose received count would overflow its buffer (heavily skewed data) or
 // a non-finite range falls back to the global path.
-constexpr int CT = 512;  // threads per cluster CTA
+constexpr int CT = 1024;  // threads per cluster CTA
+constexpr int NWARP = CT / 32;
+constexpr int EMAX = 16;         // slice elements per thread (slice <= 16K)
+constexpr int kIdxBits = 18;     // row within the block (< 2^18) | local bucket in the high bits
+constexpr uint32_t kIdxMask = (1u << kIdxBits) - 1u;
 constexpr int kMaxCluster = 16;
-constexpr size_t kSmemLimit = 227 * 1024 - 4096;  // leave room for static shared memory
+constexpr size_t kSmemLimit = 227 * 1024 - 8192;  // leave room for static shared memory
 
 struct ClusterJob {
     uint64_t begin;
@@ -366,7 +371,7 @@ struct ClusterPlan {
     int cl = 0;            // CTAs per cluster (0: no cluster path)
     uint32_t s = 0;        // max slice
     uint32_t rcap = 0;     // receive capacity per CTA
-    uint32_t nbl = 0;      // local buckets per CTA
+    uint32_t lg_nbl = 0;   // log2 local buckets per CTA
     size_t smem = 0;
 };
 
@@ -381,8 +386,11 @@ inline ClusterPlan plan_for(uint64_t nmax, int cl) {
     p.s = static_cast<uint32_t>((nmax + cl - 1) / cl);
     const uint32_t slack = std::max<uint32_t>(256u, static_cast<uint32_t>(6.0 * std::sqrt(static_cast<double>(p.s))));
     p.rcap = (p.s + slack + 31u) & ~31u;
-    p.nbl = std::max<uint32_t>(1u, p.s / 6);
-    p.smem = static_cast<size_t>(p.rcap) * 14 + static_cast<size_t>(p.nbl) * 8 + 64;
+    uint32_t lg = 1;
+    while ((2u << lg) <= std::max<uint32_t>(2u, p.s / 2)) ++lg;  // NBL = largest power of two <= S/2 (>= 2)
+    p.lg_nbl = lg;
+    // recv key 8 + row 4 + perm 2 per slot; NBL u16 counters/cursors + NBL+2 u16 starts
+    p.smem = static_cast<size_t>(p.rcap) * 14 + (static_cast<size_t>(1u << lg) * 2 + 4) * 2 + 64;
     return p;
 }
 
@@ -392,27 +400,71 @@ inline ClusterPlan plan_cluster(uint64_t nmax) {
     for (int cl = 1; cl <= kMaxCluster; ++cl) {
         if (forced && cl != forced) continue;
         ClusterPlan p = plan_for(nmax, cl);
-        if (p.rcap < 65535 && p.smem <= kSmemLimit) return p;
+        if (p.rcap < 65535 && p.smem <= kSmemLimit && p.s <= static_cast<uint32_t>(EMAX * CT) &&
+            nmax <= kIdxMask && (p.lg_nbl + kIdxBits) <= 32 && (static_cast<uint64_t>(cl) << p.lg_nbl) <= 65536)
+            return p;
     }
     return ClusterPlan{};
 }
 
-__device__ __forceinline__ uint32_t agg_add(uint32_t* base, uint32_t key, bool valid) {
-    const unsigned active = __ballot_sync(0xffffffffu, valid);
-    if (!valid) return 0u;
-    const unsigned peers = __match_any_sync(active, key);
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(peers) - 1;
-    uint32_t b = 0;
-    if (lane == leader) b = atomicAdd(base + key, static_cast<uint32_t>(__popc(peers)));
-    b = __shfl_sync(peers, b, leader);
-    return b + static_cast<uint32_t>(__popc(peers & ((1u << lane) - 1u)));
+__device__ __forceinline__ uint32_t cbucket(unsigned long long k, double hm, double scale, uint32_t nbtot) {
+    const double t = (0.5 * key_value(k) - hm) * scale;
+    return t < static_cast<double>(nbtot) ? static_cast<uint32_t>(t) : nbtot - 1u;
+}
+
+// Same scan over NBL u16 counters packed two per word (`cw`); writes the u16
+// starts (start[n] = total) and turns cw into cursors (packed starts).
+__device__ void block_scan_excl_u16(uint32_t* cw, uint16_t* start, uint32_t n, uint32_t* s_w) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t nw = n / 2;
+    const uint32_t per = (nw + CT - 1) / CT;
+    const uint32_t b0 = min(nw, tid * per), b1 = min(nw, b0 + per);
+    uint32_t loc = 0;
+    for (uint32_t q = b0; q < b1; ++q) loc += (cw[q] & 0xffffu) + (cw[q] >> 16);
+    uint32_t x = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t z = lane < NWARP ? s_w[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += y;
+        }
+        if (lane < NWARP) s_w[lane] = z;
+    }
+    __syncthreads();
+    uint32_t run = (wid ? s_w[wid - 1] : 0u) + x - loc;
+    for (uint32_t q = b0; q < b1; ++q) {
+        const uint32_t w = cw[q];
+        const uint32_t s0 = run, s1 = run + (w & 0xffffu);
+        start[2 * q] = static_cast<uint16_t>(s0);
+        start[2 * q + 1] = static_cast<uint16_t>(s1);
+        cw[q] = s0 | (s1 << 16);
+        run = s1 + (w >> 16);
+    }
+    if (tid == CT - 1) start[n] = static_cast<uint16_t>(run);
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, const double* c0, const double* c1,
                                                        uint64_t n_rows, unsigned long long* rp, int32_t* fb,
-                                                       int32_t* bad, int CL, uint32_t RCAP, uint32_t NBL) {
+                                                       int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
+                                                       unsigned long long* prof) {
     namespace cg = cooperative_groups;
+    long long t_prev = clock64();
+    auto mark = [&](int k) {  // optional phase timing (PCB_RANK_PROFILE): thread 0's clock deltas
+        if (prof && threadIdx.x == 0) {
+            const long long t = clock64();
+            atomicAdd(prof + k, static_cast<unsigned long long>(t - t_prev));
+            t_prev = t;
+        }
+    };
     cg::cluster_group cluster = cg::this_cluster();
     const int r = static_cast<int>(cluster.block_rank());
     const uint32_t jid = blockIdx.x / CL;
@@ -421,31 +473,37 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     const uint32_t S = (J.n + CL - 1) / CL;
     const uint32_t a = min(J.n, r * S), e = min(J.n, a + S);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t NBL = 1u << lg_nbl;
 
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* recv_key = reinterpret_cast<unsigned long long*>(smem);
     uint32_t* recv_idx = reinterpret_cast<uint32_t*>(recv_key + RCAP);
-    uint32_t* lh_cnt = recv_idx + RCAP;
-    uint32_t* lh_start = lh_cnt + NBL;
-    uint16_t* perm = reinterpret_cast<uint16_t*>(lh_start + NBL);
+    uint32_t* lhw = recv_idx + RCAP;                            // NBL u16 counts -> cursors, two per word
+    uint16_t* lhs = reinterpret_cast<uint16_t*>(lhw + NBL / 2);  // NBL+1 u16 starts (+1 pad)
+    uint16_t* perm = lhs + NBL + 2;
 
-    __shared__ unsigned long long s_kmin[CT / 32], s_kmax[CT / 32];
-    __shared__ unsigned long long s_rmin, s_rmax;  // this CTA's reduced extremes (read remotely)
-    __shared__ int s_bad;
-    __shared__ uint32_t s_cnt[kMaxCluster];   // elements this CTA sends to each peer (read remotely)
-    __shared__ uint32_t s_cur[kMaxCluster];   // send cursors
+    __shared__ unsigned long long s_k[2][NWARP];
+    __shared__ unsigned long long s_rmin, s_rmax, s_gmin, s_gmax;  // s_rmin/s_rmax are read by peers
+    __shared__ int s_bad, s_gbad, s_over;
+    __shared__ uint32_t s_wc[NWARP][kMaxCluster];  // per-warp counts -> per-warp send cursors
+    __shared__ uint32_t s_cnt[kMaxCluster];         // this CTA's sends per owner (read by peers)
     __shared__ uint32_t s_mat[kMaxCluster * kMaxCluster];
-    __shared__ uint32_t s_warp[CT / 32];
+    __shared__ uint32_t s_off[kMaxCluster], s_total, s_base;
+    __shared__ uint32_t s_w[NWARP];
 
-    // ---- 1. slice extremes
+    // ---- 1. slice extremes (all EMAX loads of a thread in flight together)
     unsigned long long kmn = ~0ull, kmx = 0ull;
     bool fin = true;
-    for (uint32_t i = a + tid; i < e; i += CT) {
-        const double v = x[i];
-        fin &= isfinite(v);
-        const unsigned long long k = order_key(v);
-        kmn = min(kmn, k);
-        kmx = max(kmx, k);
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k) {
+        const uint32_t i = a + k * CT + tid;
+        if (i < e) {
+            const double v = x[i];
+            fin &= isfinite(v);
+            const unsigned long long kk = order_key(v);
+            kmn = min(kmn, kk);
+            kmx = max(kmx, kk);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -454,25 +512,24 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     }
     fin = __all_sync(0xffffffffu, fin);
     if (tid == 0) s_bad = 0;
-    if (tid < kMaxCluster) s_cnt[tid] = 0u;
+    for (int q = tid; q < NWARP * kMaxCluster; q += CT) (&s_wc[0][0])[q] = 0u;
     __syncthreads();
     if (lane == 0) {
-        s_kmin[wid] = kmn;
-        s_kmax[wid] = kmx;
+        s_k[0][wid] = kmn;
+        s_k[1][wid] = kmx;
         if (!fin) s_bad = 1;
     }
     __syncthreads();
     if (tid == 0) {
-        for (int w = 1; w < CT / 32; ++w) {
-            kmn = min(kmn, s_kmin[w]);
-            kmx = max(kmx, s_kmax[w]);
+        for (int w = 1; w < NWARP; ++w) {
+            kmn = min(kmn, s_k[0][w]);
+            kmx = max(kmx, s_k[1][w]);
         }
         s_rmin = kmn;
         s_rmax = kmx;
     }
     cluster.sync();
-    __shared__ unsigned long long s_gmin, s_gmax;
-    __shared__ int s_gbad;
+    mark(0);
     if (tid == 0) {
         unsigned long long gmn = ~0ull, gmx = 0ull;
         int gb = 0;
@@ -486,58 +543,65 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
         s_gbad = gb;
     }
     __syncthreads();
-    const unsigned long long gmin = s_gmin, gmax = s_gmax;
-    const double vmin = key_value(gmin), vmax = key_value(gmax);
+    const double vmin = key_value(s_gmin), vmax = key_value(s_gmax);
     const double hm = 0.5 * vmin;
-    const double nbt = static_cast<double>(CL) * static_cast<double>(NBL);
-    const double scale = nbt / (0.5 * vmax - hm);
-    const bool constant = gmin == gmax;
+    const uint32_t nbtot = static_cast<uint32_t>(CL) << lg_nbl;
+    const double scale = static_cast<double>(nbtot) / (0.5 * vmax - hm);
+    const bool constant = s_gmin == s_gmax;
     if (s_gbad || constant || !(isfinite(scale) && scale > 0.0 && isfinite(hm))) {
         if (s_gbad) {
             if (r == 0 && tid == 0) bad[J.seg] = 1;
         } else if (constant) {  // one tie run: avg rank (n+1)/2 for all, stable positions = row order
             for (uint32_t i = a + tid; i < e; i += CT)
-                rp[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = pack_rank(J.n + 1u, i);
+                rp[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = pack_rank(J.n + 1u, i, i == 0);
         } else if (r == 0 && tid == 0) {
             fb[jid] = 1;
         }
         cluster.sync();  // peers may still be reading this CTA's shared memory
         return;
     }
-    const uint32_t nbtot = static_cast<uint32_t>(CL) * NBL;
-    auto bucket = [&](unsigned long long k) -> uint32_t {
-        const double t = (0.5 * key_value(k) - hm) * scale;
-        return t < static_cast<double>(nbtot) ? static_cast<uint32_t>(t) : nbtot - 1u;
-    };
 
-    // ---- 2. counts to each value-range owner
-    const uint32_t iters = (e - a + CT - 1) / CT;
-    for (uint32_t it = 0; it < iters; ++it) {
-        const uint32_t i = a + it * CT + tid;
-        const bool valid = i < e;
-        uint32_t d = 0;
-        if (valid) d = bucket(order_key(x[i])) / NBL;
-        agg_add(s_cnt, d, valid);
+    // ---- 2. per-warp counts of what this CTA sends to each value-range owner;
+    // each element's global bucket is kept (16 bits, two per register)
+    uint32_t bk[(EMAX + 1) / 2];
+#pragma unroll
+    for (int k = 0; k < (EMAX + 1) / 2; ++k) bk[k] = 0u;
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k) {
+        const uint32_t i = a + k * CT + tid;
+        if (i < e) {
+            const uint32_t b = cbucket(order_key(x[i]), hm, scale, nbtot);
+            bk[k >> 1] |= b << ((k & 1) * 16);
+            atomicAdd(&s_wc[wid][b >> lg_nbl], 1u);
+        }
+    }
+    __syncthreads();
+    if (tid < CL) {  // totals per owner, and per-warp exclusive bases
+        uint32_t run = 0;
+        for (int w = 0; w < NWARP; ++w) {
+            const uint32_t c = s_wc[w][tid];
+            s_wc[w][tid] = run;
+            run += c;
+        }
+        s_cnt[tid] = run;
     }
     cluster.sync();
+    mark(1);
     if (tid < CL * CL) s_mat[tid] = *cluster.map_shared_rank(&s_cnt[tid % CL], tid / CL);  // [src][dst]
     __syncthreads();
-    __shared__ uint32_t s_total, s_base;
-    __shared__ int s_over;
     if (tid == 0) {
         int over = 0;
         uint32_t base = 0, total = 0;
         for (int d = 0; d < CL; ++d) {
-            uint32_t col = 0;
-            for (int q = 0; q < CL; ++q) col += s_mat[q * CL + d];
+            uint32_t col = 0, mine = 0;
+            for (int q = 0; q < CL; ++q) {
+                col += s_mat[q * CL + d];
+                if (q < r) mine += s_mat[q * CL + d];
+            }
+            s_off[d] = mine;
             if (col > RCAP) over = 1;
             if (d < r) base += col;
             if (d == r) total = col;
-        }
-        for (int d = 0; d < CL; ++d) {
-            uint32_t o = 0;
-            for (int q = 0; q < r; ++q) o += s_mat[q * CL + d];
-            s_cur[d] = o;
         }
         s_total = total;
         s_base = base;
@@ -547,83 +611,56 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     if (s_over) {
         if (r == 0 && tid == 0) fb[jid] = 1;
         cluster.sync();
+        mark(2);
         return;
     }
+    for (int q = tid; q < NWARP * CL; q += CT) s_wc[q / CL][q % CL] += s_off[q % CL];
+    __syncthreads();
 
-    // ---- 3. scatter (key, row) to the owners (DSMEM stores)
-    for (uint32_t it = 0; it < iters; ++it) {
-        const uint32_t i = a + it * CT + tid;
-        const bool valid = i < e;
-        unsigned long long k = 0;
-        uint32_t d = 0;
-        if (valid) {
-            k = order_key(x[i]);
-            d = bucket(k) / NBL;
-        }
-        const uint32_t slot = agg_add(s_cur, d, valid);
-        if (valid) {
-            *cluster.map_shared_rank(recv_key + slot, d) = k;
-            *cluster.map_shared_rank(recv_idx + slot, d) = i;
+    // ---- 3. scatter (key, local bucket | row) to the owners (DSMEM stores)
+    const uint32_t lmask = NBL - 1u;
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k) {
+        const uint32_t i = a + k * CT + tid;
+        if (i < e) {
+            const unsigned long long kk = order_key(x[i]);
+            const uint32_t b = (bk[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
+            const uint32_t d = b >> lg_nbl;
+            const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
+            *cluster.map_shared_rank(recv_key + slot, d) = kk;
+            *cluster.map_shared_rank(recv_idx + slot, d) = ((b & lmask) << kIdxBits) | i;
         }
     }
-    cluster.sync();  // all stores into every receive buffer are visible; no remote access after this
+    cluster.sync();  // every receive buffer is complete; no DSMEM access after this point
+    mark(3);
 
     // ---- 4. local counting sort into NBL buckets
     const uint32_t T = s_total, base = s_base;
-    const uint32_t b0 = static_cast<uint32_t>(r) * NBL;
-    for (uint32_t q = tid; q < NBL; q += CT) lh_cnt[q] = 0u;
+    for (uint32_t q = tid; q < NBL / 2; q += CT) lhw[q] = 0u;
     __syncthreads();
-    for (uint32_t j = tid; j < T; j += CT) atomicAdd(lh_cnt + (bucket(recv_key[j]) - b0), 1u);
-    __syncthreads();
-    // exclusive scan lh_cnt -> lh_start (block scan in chunks of CT)
-    __shared__ uint32_t s_carry;
-    if (tid == 0) s_carry = 0u;
-    __syncthreads();
-    for (uint32_t q0 = 0; q0 < NBL; q0 += CT) {
-        const uint32_t q = q0 + tid;
-        const uint32_t v = q < NBL ? lh_cnt[q] : 0u;
-        uint32_t x2 = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x2, o);
-            if (lane >= o) x2 += y;
-        }
-        if (lane == 31) s_warp[wid] = x2;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t z = lane < CT / 32 ? s_warp[lane] : 0u;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
-                if (lane >= o) z += y;
-            }
-            if (lane < CT / 32) s_warp[lane] = z;
-        }
-        __syncthreads();
-        const uint32_t excl = s_carry + (wid ? s_warp[wid - 1] : 0u) + x2 - v;
-        if (q < NBL) {
-            lh_start[q] = excl;
-            lh_cnt[q] = excl;  // cursor
-        }
-        __syncthreads();
-        if (tid == CT - 1) s_carry = excl + v;
-        __syncthreads();
-    }
     for (uint32_t j = tid; j < T; j += CT) {
-        const uint32_t slot = atomicAdd(lh_cnt + (bucket(recv_key[j]) - b0), 1u);
+        const uint32_t lb = recv_idx[j] >> kIdxBits;
+        atomicAdd(lhw + (lb >> 1), 1u << ((lb & 1) * 16));
+    }
+    __syncthreads();
+    block_scan_excl_u16(lhw, lhs, NBL, s_w);  // counts < 2^16: a bucket never exceeds RCAP < 65535
+    for (uint32_t j = tid; j < T; j += CT) {
+        const uint32_t lb = recv_idx[j] >> kIdxBits, sh = (lb & 1) * 16;
+        const uint32_t slot = (atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu;
         perm[slot] = static_cast<uint16_t>(j);
     }
     __syncthreads();
 
-    // ---- 5. rank inside each bucket; write packed (r2 | pos)
+    mark(4);
+    // ---- 5. rank inside each bucket; write packed (r2 | pos | run-start)
     unsigned long long* out = rp + static_cast<uint64_t>(J.col) * n_rows + J.begin;
     for (uint32_t j = tid; j < T; j += CT) {
         const unsigned long long k = recv_key[j];
-        const uint32_t id = recv_idx[j];
-        const uint32_t lb = bucket(k) - b0;
-        const uint32_t s0 = lh_start[lb];
-        const uint32_t s1 = lb + 1 < NBL ? lh_start[lb + 1] : T;
+        const uint32_t id = recv_idx[j];  // (local bucket << kIdxBits) | row: same bucket => compares as row
+        const uint32_t lb = id >> kIdxBits;
+        const uint32_t s0 = lhs[lb], s1 = lhs[lb + 1];
         uint32_t less = 0, same = 0, before = 0;
+#pragma unroll 1
         for (uint32_t q = s0; q < s1; ++q) {
             const uint32_t o = perm[q];
             const unsigned long long kq = recv_key[o];
@@ -633,8 +670,9 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
             before += eqk && recv_idx[o] < id;
         }
         const uint32_t lt = base + s0 + less;
-        out[id] = pack_rank(2u * lt + same + 1u, lt + before);
+        out[id & kIdxMask] = pack_rank(2u * lt + same + 1u, lt + before, before == 0);
     }
+    mark(5);
 }
 
 void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, uint32_t njobs, const double* c0,
@@ -654,7 +692,22 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, rp, fb, bad, p.cl, p.rcap, p.nbl));
+    unsigned long long* prof = nullptr;
+    if (getenv_flag("PCB_RANK_PROFILE")) {
+        prof = c.ws.get_t<unsigned long long>("rank.prof", 8);
+        PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
+    }
+    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, rp, fb, bad, p.cl, p.rcap, p.lg_nbl,
+                                prof));
+    if (prof) {
+        unsigned long long h[8];
+        PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+        const double ctas = static_cast<double>(njobs) * p.cl;
+        std::fprintf(stderr, "[rank profile] CL=%d S=%u: cycles/CTA  minmax %.0f  count %.0f  matrix %.0f  send %.0f  "
+                     "localsort %.0f  rank %.0f\n", p.cl, p.s, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
+                     h[4] / ctas, h[5] / ctas);
+    }
     c.count_launch();
 }
 

@@ -172,9 +172,10 @@ class Context:
         return int(self.lib.pcb_launch_count(self.ptr))
 
     def stage_times(self) -> dict:
-        buf = (C.c_double * 8)()
-        k = self.lib.pcb_stage_times(self.ptr, buf, 8)
-        names = ["rank", "prepare", "newton", "variance", "finalize", "lik_kernel_ms", "lik_launches"]
+        buf = (C.c_double * 12)()
+        k = self.lib.pcb_stage_times(self.ptr, buf, 12)
+        names = ["rank", "prepare", "newton", "variance", "finalize", "lik_kernel_ms", "lik_launches",
+                 "warm_kernel_ms", "warm_launches"]
         return {names[i]: float(buf[i]) for i in range(k)}
 
     def trim(self):
