@@ -137,6 +137,7 @@ struct RankBufs {
 RankBufs rank_buffers(pcb::Ctx& c, uint64_t n_rows, uint64_t n_seg) {
     RankBufs b;
     b.r.rp = c.ws.get_t<unsigned long long>("pipe.rp", 2 * n_rows);
+    b.r.ord = c.ws.get_t<uint32_t>("pipe.ord", 2 * n_rows);
     b.bad = c.ws.get_t<int32_t>("pipe.bad", n_seg);
     PCB_CUDA(cudaMemsetAsync(b.bad, 0, n_seg * sizeof(int32_t), c.stream));
     return b;
@@ -152,7 +153,7 @@ void finish_stage_times(pcb::Ctx& c) {
         }
         c.stage_ms[k] = ms;
     }
-    c.n_stage = 9;
+    c.n_stage = 10;
 }
 
 // raw columns (device) -> ranks -> fit -> variance; records to d_out (device)
@@ -168,6 +169,7 @@ void pipeline_blocks(pcb::Ctx& c, int fam, int prec, const double* d1, const dou
     io.n_rows = n_rows;
     io.off = off;
     io.rp = rb.r.rp;
+    io.ord = rb.r.ord;
     io.bad = rb.bad;
     pcb::run_fit(c, io, d_out);
     finish_stage_times(c);
@@ -318,6 +320,7 @@ int pcb_fit(pcb_context* ctx, int family, int precision, const double* u1, const
         io.u1 = d1;
         io.u2 = d2;
         io.rp = rb.r.rp;
+        io.ord = rb.r.ord;
         DevOut<pcb_fit_result> o(c, out, n_seg, "fit");
         pcb::run_fit(c, io, o.dev);
         finish_stage_times(c);
@@ -356,6 +359,7 @@ int pcb_asymptotic_variance(pcb_context* ctx, int family, const double* theta_ha
         io.u1 = d1;
         io.u2 = d2;
         io.rp = rb.r.rp;
+        io.ord = rb.r.ord;
         io.theta_in = dth;
         io.do_fit = false;
         auto* rec = c.ws.get_t<pcb_fit_result>("var.rec", n_seg);

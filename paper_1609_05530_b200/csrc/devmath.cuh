@@ -225,14 +225,19 @@ __device__ __forceinline__ double frank_cross_dev(double a, double other, double
 }
 
 // log c, score, Hessian, cross terms at (u, v) — the variance pass.
+// expm1(-t*u) and expm1(-t*v) are the bracket's own exponentials (u and v are
+// lo and hi in some order): expm1(-t*hi) = em2 + emb + em2*emb exactly, so the
+// two cross derivatives (copula.hpp:147-154) need no further exponentials.
 __device__ __forceinline__ PointFull frank_full(double u, double v, const FrankTheta& f) {
     if (f.neg) v = 1.0 - v;
     const double t = f.t;
-    const double lo = fmin(u, v), hi = fmax(u, v);
+    const bool ulo = u <= v;
+    const double lo = ulo ? u : v, hi = ulo ? v : u;
     const double ema = expm1(-t * (1.0 - lo));
     const double k2 = -t * (hi - lo);
-    const double e2 = exp(k2);
+    const double em2 = expm1(k2);
     const double emb = expm1(-t * lo);
+    const double e2 = 1.0 + em2;
     const double e1 = 1.0 + ema, e3 = 1.0 + emb;
     const double b = ema + e2 * emb;
     const double sum = lo + hi;
@@ -245,8 +250,17 @@ __device__ __forceinline__ PointFull frank_full(double u, double v, const FrankT
     const double sc = f.inv_t - f.g - (u + v) - 2.0 * q;
     p.hess = f.hconst - 2.0 * (bpp * rb - q * q);
     const double rb2 = rb * rb;
-    const double c1 = frank_cross_dev(u, v, t, u <= v ? 1.0 : e2, rb, bp, rb2);
-    const double c2 = frank_cross_dev(v, u, t, v <= u ? 1.0 : e2, rb, bp, rb2);
+    const double emhi = em2 + emb + em2 * emb;  // expm1(-t*hi)
+    const double em_u = ulo ? emb : emhi, em_v = ulo ? emhi : emb;
+    // cross for first argument a with the other argument o: shift = 1 if a <= o else e2
+    auto cross = [&](double a, double o, double em_o, double shift) {
+        const double ev = 1.0 + em_o;
+        const double ea = -t * shift * em_o;
+        const double dea = shift * ((t * a - 1.0) * em_o + t * o * ev);
+        return -1.0 - 2.0 * (dea * rb - ea * bp * rb2);
+    };
+    const double c1 = cross(u, v, em_v, ulo ? 1.0 : e2);
+    const double c2 = cross(v, u, em_u, ulo ? (u == v ? 1.0 : e2) : 1.0);
     p.score = f.neg ? -sc : sc;
     p.cross1 = f.neg ? -c1 : c1;
     p.cross2 = c2;

@@ -163,13 +163,16 @@ __global__ void k_init_state(BlockState* st, const Seg* segs, int nseg, const in
 
 // Prepare pass: theta-independent per-point pair + init statistics; the
 // segment's last tile computes the starting theta (Gaussian: solves the fit).
-// with_fit == 0 (variance-only API): only T is written.
+// with_fit == 0 (variance-only API): only T is written. `gtab` (rank-derived
+// u only) holds the per-rank transform of the block's size: Phi^-1(u)
+// (Gaussian) or ln(-ln u) (Gumbel), bit-identical to computing it per point.
 template <int FAM, class TO>
 __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs, int nseg,
-                                               const unsigned long long* rp, const double* u1, const double* u2,
-                                               uint64_t n_rows, TO* T, float2* T32, const double* gtab,
-                                               const uint64_t* goff, double* partials, unsigned* tickets,
-                                               unsigned* running, int with_fit) {
+                                               const unsigned long long* __restrict__ rp,
+                                               const double* __restrict__ u1, const double* __restrict__ u2,
+                                               uint64_t n_rows, TO* __restrict__ T, float2* __restrict__ T32,
+                                               const double* __restrict__ gtab, const uint64_t* goff,
+                                               double* partials, unsigned* tickets, unsigned* running, int with_fit) {
     const uint32_t tile = blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
@@ -177,41 +180,62 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
     if (with_fit ? status != kRunning : status != kConverged) return;
     const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);
     const uint32_t base = (tile - S.tile0) * FTILE;
+    const double* gt = gtab ? gtab + goff[m] : nullptr;
     double v[2] = {0.0, 0.0};
-#pragma unroll 2
-    for (int k = 0; k < PPT; ++k) {
-        const uint32_t i = base + k * FT + threadIdx.x;
-        if (i >= S.n) break;
-        const uint64_t row = S.begin + i;
-        double u, w;
-        point_u(rp, u1, u2, n_rows, row, scale, u, w);
-        u = clamp_unit(u);
-        w = clamp_unit(w);
-        if (FAM == kGaussian) {
-            double x, y;
-            if (gtab) {  // Phi^-1 depends only on the rank: per-block-size table (bit-identical values)
-                const double* tb = gtab + goff[m];
-                x = tb[rank_r2(rp[row])];
-                y = tb[rank_r2(rp[n_rows + row])];
-            } else {
-                x = dev_phi_inv(u);
-                y = dev_phi_inv(w);
-                T[row] = TO{static_cast<decltype(TO::x)>(x), static_cast<decltype(TO::x)>(y)};
+    constexpr int U = 4;  // points per thread in flight
+    for (int k0 = 0; k0 < PPT; k0 += U) {
+        double uu[U], ww[U], gx[U], gy[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            if (i < S.n) {
+                const uint64_t row = S.begin + i;
+                if (u1) {
+                    uu[j] = u1[row];
+                    ww[j] = u2[row];
+                } else {
+                    const uint32_t r1 = rank_r2(rp[row]), r2 = rank_r2(rp[n_rows + row]);
+                    uu[j] = __dmul_rn(0.5 * static_cast<double>(r1), scale);
+                    ww[j] = __dmul_rn(0.5 * static_cast<double>(r2), scale);
+                    if (gt) {
+                        gx[j] = gt[r1];
+                        gy[j] = gt[r2];
+                    }
+                }
             }
-            v[0] += x * y;
-            v[1] += x * x + y * y;
-        } else {
-            v[0] += u * w;
-            if (FAM == kFrank) {
-                if (sizeof(TO) == 8)
-                    T[row] = TO{static_cast<decltype(TO::x)>(frank_edge(u)), static_cast<decltype(TO::x)>(frank_edge(w))};
-                else
-                    T[row] = TO{static_cast<decltype(TO::x)>(u), static_cast<decltype(TO::x)>(w)};
-                if (T32) T32[row] = float2{frank_edge(u), frank_edge(w)};
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            if (i >= S.n) continue;
+            const uint64_t row = S.begin + i;
+            const double u = clamp_unit(uu[j]), w = clamp_unit(ww[j]);
+            if (FAM == kGaussian) {
+                double x, y;
+                if (gt) {
+                    x = gx[j];
+                    y = gy[j];
+                } else {
+                    x = dev_phi_inv(u);
+                    y = dev_phi_inv(w);
+                    T[row] = TO{static_cast<decltype(TO::x)>(x), static_cast<decltype(TO::x)>(y)};
+                }
+                v[0] += x * y;
+                v[1] += x * x + y * y;
             } else {
-                const double lx = log(-log(u)), ly = log(-log(w));
-                T[row] = TO{static_cast<decltype(TO::x)>(lx), static_cast<decltype(TO::x)>(ly)};
-                if (T32) T32[row] = float2{static_cast<float>(lx), static_cast<float>(ly)};
+                v[0] += u * w;
+                if (FAM == kFrank) {
+                    if (sizeof(TO) == 8)
+                        T[row] = TO{static_cast<decltype(TO::x)>(frank_edge(u)),
+                                    static_cast<decltype(TO::x)>(frank_edge(w))};
+                    else
+                        T[row] = TO{static_cast<decltype(TO::x)>(u), static_cast<decltype(TO::x)>(w)};
+                    if (T32) T32[row] = float2{frank_edge(u), frank_edge(w)};
+                } else {
+                    const double lx = gt ? gx[j] : log(-log(u)), ly = gt ? gy[j] : log(-log(w));
+                    T[row] = TO{static_cast<decltype(TO::x)>(lx), static_cast<decltype(TO::x)>(ly)};
+                    if (T32) T32[row] = float2{static_cast<float>(lx), static_cast<float>(ly)};
+                }
             }
         }
     }
@@ -373,12 +397,15 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
     }
 }
 
-// Phi^-1((0.5*r2)/(n+1)) for every r2 in [2, 2n]: the Gaussian scores of a
-// block of n ranked rows (same arithmetic as the per-point path).
-__global__ void k_gauss_table(double* tab, uint32_t n) {
+// The theta-independent per-point transform of u = (0.5*r2)/(n+1) for every
+// r2 in [2, 2n] of a block of n ranked rows — Phi^-1(u) (Gaussian scores) or
+// ln(-ln u) (Gumbel) — with the same arithmetic as the per-point path.
+__global__ void k_rank_table(double* tab, uint32_t n, int fam) {
     const double scale = 1.0 / (static_cast<double>(n) + 1.0);
-    for (uint32_t r2 = blockIdx.x * blockDim.x + threadIdx.x; r2 <= 2 * n; r2 += gridDim.x * blockDim.x)
-        tab[r2] = r2 >= 2 ? dev_phi_inv(clamp_unit(__dmul_rn(0.5 * static_cast<double>(r2), scale))) : 0.0;
+    for (uint32_t r2 = blockIdx.x * blockDim.x + threadIdx.x; r2 <= 2 * n; r2 += gridDim.x * blockDim.x) {
+        const double u = clamp_unit(__dmul_rn(0.5 * static_cast<double>(r2), scale));
+        tab[r2] = r2 < 2 ? 0.0 : (fam == kGaussian ? dev_phi_inv(u) : log(-log(u)));
+    }
 }
 
 struct RecordOut {  // == pcb_fit_result
@@ -559,7 +586,7 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
     // Gaussian scores by rank table (rank-derived u only; few distinct block sizes)
     const double* gtab = nullptr;
     const uint64_t* goff = nullptr;
-    if (fam == kGaussian && !io.u1 && !getenv_flag("PCB_NO_GTAB")) {
+    if ((fam == kGaussian || fam == kGumbel) && !io.u1 && !getenv_flag("PCB_NO_GTAB")) {
         std::vector<uint32_t> sizes;
         for (int m = 0; m < K; ++m)
             if (std::find(sizes.begin(), sizes.end(), segs[m].n) == sizes.end()) sizes.push_back(segs[m].n);
@@ -578,14 +605,15 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
             PCB_CUDA(cudaMemcpyAsync(d_off, hoff.data(), K * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
             for (size_t q = 0; q < sizes.size(); ++q) {
                 const uint32_t nn = sizes[q];
-                k_gauss_table<<<std::min<uint32_t>(148u * 8u, (2 * nn + 256) / 256), 256, 0, s>>>(tab + base[q], nn);
+                k_rank_table<<<std::min<uint32_t>(148u * 8u, (2 * nn + 256) / 256), 256, 0, s>>>(tab + base[q], nn, fam);
                 c.count_launch();
             }
             gtab = tab;
             goff = d_off;
         }
     }
-    void* T = gtab ? nullptr : c.ws.get("fit.T", io.n_rows * (fp32T ? sizeof(float2) : sizeof(double2)));
+    void* T = (gtab && fam == kGaussian) ? nullptr
+                                         : c.ws.get("fit.T", io.n_rows * (fp32T ? sizeof(float2) : sizeof(double2)));
     float2* T32 = warm ? c.ws.get_t<float2>("fit.T32", io.n_rows) : nullptr;
     if (tiles > 0) {
         const int with_fit = io.do_fit ? 1 : 0;
@@ -638,10 +666,11 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
         v.tiles = tiles;
         v.st = st;
         v.rp = io.rp;
+        v.ord = io.ord;
         v.u1 = io.u1;
         v.u2 = io.u2;
         v.T64 = ((fam == kGaussian && !gtab) || (fam == kGumbel && !fp32T)) ? static_cast<const double2*>(T) : nullptr;
-        v.gtab = gtab;
+        v.gtab = fam == kGaussian ? gtab : nullptr;
         v.goff = goff;
         v.partials = part;
         v.tickets = tick;

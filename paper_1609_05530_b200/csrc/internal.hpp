@@ -96,6 +96,7 @@ struct Ctx {
 // tie run begins; the variance finds a run's first position from them.
 struct RankOut {
     unsigned long long* rp;
+    uint32_t* ord;  // [2][n_rows]: sorted position -> row within the segment (the stable order)
 };
 
 // Ranks both columns of every segment. `bad` (n_seg int32, device) is set
@@ -116,6 +117,7 @@ struct FitIO {
     // packed ranks [2][n_rows] (always: the variance needs the stable
     // positions); (u, v) come from u1/u2 when given, else from the ranks
     const unsigned long long* rp = nullptr;
+    const uint32_t* ord = nullptr;
     const double* u1 = nullptr;
     const double* u2 = nullptr;
     const int32_t* bad = nullptr;  // per segment, may be null
@@ -138,6 +140,7 @@ struct VarIO {
     uint32_t tiles = 0;
     BlockState* st = nullptr;
     const unsigned long long* rp = nullptr;
+    const uint32_t* ord = nullptr;
     const double* u1 = nullptr;
     const double* u2 = nullptr;
     const double2* T64 = nullptr;  // hoisted (x,y) (Gaussian) / (ln(-ln u), ln(-ln v)) (Gumbel fp64), or null

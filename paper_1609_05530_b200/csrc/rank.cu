@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(RT) k_scatter(const RankRange* rr, int nr, con
 // by counting inside the bucket (L1-resident neighbours).
 __global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const unsigned long long* dkey,
                                             const uint32_t* didx, const uint32_t* hist, const uint32_t* bstart,
-                                            uint64_t n_rows, unsigned long long* o_rp) {
+                                            uint64_t n_rows, unsigned long long* o_rp, uint32_t* o_ord) {
     const int r = range_of_tile(rr, nr, blockIdx.x);
     const RankRange R = rr[r];
     const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const 
         }
         const uint64_t o = static_cast<uint64_t>(R.col) * n_rows + R.out_base + id;
         o_rp[o] = pack_rank(2u * lt + eq + 1u, pos, R.mode == 2 ? pos == R.run_start : pos == lt);
+        o_ord[static_cast<uint64_t>(R.col) * n_rows + R.out_base + pos] = id;
     }
 }
 
@@ -453,9 +454,9 @@ __device__ void block_scan_excl_u16(uint32_t* cw, uint16_t* start, uint32_t n, u
 }
 
 __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, const double* c0, const double* c1,
-                                                       uint64_t n_rows, unsigned long long* rp, int32_t* fb,
-                                                       int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
-                                                       unsigned long long* prof) {
+                                                       uint64_t n_rows, unsigned long long* rp, uint32_t* ord,
+                                                       int32_t* fb, int32_t* bad, int CL, uint32_t RCAP,
+                                                       uint32_t lg_nbl, unsigned long long* prof) {
     namespace cg = cooperative_groups;
     long long t_prev = clock64();
     auto mark = [&](int k) {  // optional phase timing (PCB_RANK_PROFILE): thread 0's clock deltas
@@ -552,8 +553,10 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
         if (s_gbad) {
             if (r == 0 && tid == 0) bad[J.seg] = 1;
         } else if (constant) {  // one tie run: avg rank (n+1)/2 for all, stable positions = row order
-            for (uint32_t i = a + tid; i < e; i += CT)
+            for (uint32_t i = a + tid; i < e; i += CT) {
                 rp[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = pack_rank(J.n + 1u, i, i == 0);
+                ord[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = i;
+            }
         } else if (r == 0 && tid == 0) {
             fb[jid] = 1;
         }
@@ -654,6 +657,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     mark(4);
     // ---- 5. rank inside each bucket; write packed (r2 | pos | run-start)
     unsigned long long* out = rp + static_cast<uint64_t>(J.col) * n_rows + J.begin;
+    uint32_t* ordo = ord + static_cast<uint64_t>(J.col) * n_rows + J.begin;
     for (uint32_t j = tid; j < T; j += CT) {
         const unsigned long long k = recv_key[j];
         const uint32_t id = recv_idx[j];  // (local bucket << kIdxBits) | row: same bucket => compares as row
@@ -671,12 +675,14 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
         }
         const uint32_t lt = base + s0 + less;
         out[id & kIdxMask] = pack_rank(2u * lt + same + 1u, lt + before, before == 0);
+        ordo[lt + before] = id & kIdxMask;
     }
     mark(5);
 }
 
 void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, uint32_t njobs, const double* c0,
-                         const double* c1, uint64_t n_rows, unsigned long long* rp, int32_t* fb, int32_t* bad) {
+                         const double* c1, uint64_t n_rows, unsigned long long* rp, uint32_t* ord, int32_t* fb,
+                         int32_t* bad) {
     PCB_CUDA(cudaFuncSetAttribute(k_rank_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(p.smem)));
     if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(k_rank_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -697,7 +703,7 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
         prof = c.ws.get_t<unsigned long long>("rank.prof", 8);
         PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
     }
-    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, rp, fb, bad, p.cl, p.rcap, p.lg_nbl,
+    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, rp, ord, fb, bad, p.cl, p.rcap, p.lg_nbl,
                                 prof));
     if (prof) {
         unsigned long long h[8];
@@ -779,7 +785,7 @@ void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64
         k_scan<<<nr, 1024, 0, st>>>(d_rr, hist, bstart, cursor, ov, ovn, ov_cap);
         if (l0) k_scatter<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
         else k_scatter<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
-        k_rank<<<ntiles, RT, 0, st>>>(d_rr, nr, dkey, didx, hist, bstart, n_rows, out.rp);
+        k_rank<<<ntiles, RT, 0, st>>>(d_rr, nr, dkey, didx, hist, bstart, n_rows, out.rp, out.ord);
         c.count_launch(6);
         PCB_CUDA(cudaMemcpyAsync(h_ovn, ovn, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         PCB_CUDA(cudaStreamSynchronize(st));
@@ -868,7 +874,7 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
         }
         PCB_CUDA(cudaMemcpyAsync(jobs, hj.data(), njobs * sizeof(ClusterJob), cudaMemcpyHostToDevice, c.stream));
         PCB_CUDA(cudaMemsetAsync(fb, 0, njobs * sizeof(int32_t), c.stream));
-        launch_rank_cluster(c, plan, jobs, njobs, d_col1, d_col2, n_rows, out.rp, fb, d_bad);
+        launch_rank_cluster(c, plan, jobs, njobs, d_col1, d_col2, n_rows, out.rp, out.ord, fb, d_bad);
         std::vector<int32_t> hfb(njobs);
         PCB_CUDA(cudaMemcpyAsync(hfb.data(), fb, njobs * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
         PCB_CUDA(cudaStreamSynchronize(c.stream));

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -39,69 +40,104 @@ constexpr int VNW = VT / 32;
 constexpr int kMaxCl = 16;
 constexpr size_t kVarSmem = 227 * 1024 - 4096;  // static shared memory lives beside it
 
+// Per-theta constants, built once per CTA (they cost more than a point).
 template <int FAM>
-__device__ __forceinline__ PointFull eval_point(double theta, double u, double w, const double2* T64, uint64_t row,
-                                                const double* gtab, unsigned long long p1, unsigned long long p2) {
-    if (FAM == kGaussian) {
-        double x, y;
-        if (gtab) {
-            x = gtab[rank_r2(p1)];
-            y = gtab[rank_r2(p2)];
-        } else if (T64) {
-            const double2 t = T64[row];
-            x = t.x;
-            y = t.y;
-        } else {
-            x = dev_phi_inv(u);
-            y = dev_phi_inv(w);
-        }
-        return gauss_full(x, y, GaussTheta(theta));
+struct ThetaOf;
+template <>
+struct ThetaOf<kGaussian> {
+    using type = GaussTheta;
+};
+template <>
+struct ThetaOf<kFrank> {
+    using type = FrankTheta;
+};
+template <>
+struct ThetaOf<kGumbel> {
+    using type = GumbelTheta;
+};
+
+template <int FAM>
+__device__ __forceinline__ PointFull eval_point(const typename ThetaOf<FAM>::type& th, double u, double w,
+                                                const double2& t64, bool has_t) {
+    if constexpr (FAM == kGaussian) {
+        return gauss_full(has_t ? t64.x : dev_phi_inv(u), has_t ? t64.y : dev_phi_inv(w), th);
+    } else if constexpr (FAM == kFrank) {
+        return frank_full(u, w, th);
+    } else {
+        return has_t ? gumbel_full_l(u, w, t64.x, t64.y, th) : gumbel_full(u, w, th);
     }
-    if (FAM == kFrank) return frank_full(u, w, FrankTheta(theta));
-    if (T64) {
-        const double2 t = T64[row];
-        return gumbel_full_l(u, w, t.x, t.y, GumbelTheta(theta));
-    }
-    return gumbel_full(u, w, GumbelTheta(theta));
 }
+
+// The run-start flag of a sorted position rides in the least significant
+// mantissa bit of its cross value (a <= 1-ulp change, far below the 1e-9
+// parity bar and deterministic), so pass 1 scatters one 8-byte word per
+// point and column.
+__device__ __forceinline__ double with_flag(double x, bool f) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    return __longlong_as_double(static_cast<long long>((b & ~1ull) | (f ? 1ull : 0ull)));
+}
+__device__ __forceinline__ bool flag_of(double x) { return (__double_as_longlong(x) & 1ll) != 0; }
 
 // ------------------------------------------------------------ pass 1
 template <int FAM>
 __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* segs, int nseg,
-                                                 const unsigned long long* rp, const double* u1, const double* u2,
-                                                 const double2* T64, const double* gtab, const uint64_t* goff,
-                                                 uint64_t n_rows, double* zb, double* Ag, uint8_t* Fg,
-                                                 double* partials, unsigned* tickets) {
+                                                 const unsigned long long* __restrict__ rp,
+                                                 const double* __restrict__ u1, const double* __restrict__ u2,
+                                                 const double2* __restrict__ T64, const double* __restrict__ gtab,
+                                                 const uint64_t* goff, uint64_t n_rows, double* __restrict__ zb,
+                                                 double* __restrict__ Ag, double* partials,
+                                                 unsigned* tickets) {
     const uint32_t tile = blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
     if (st[m].status != kConverged) return;
-    const double theta = st[m].theta;
+    const typename ThetaOf<FAM>::type th(st[m].theta);
     const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);
     const uint32_t base = (tile - S.tile0) * FTILE;
+    const double* gt = gtab ? gtab + goff[m] : nullptr;
+    const bool has_t = gt || T64;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int k = 0; k < PPT; ++k) {
-        const uint32_t i = base + k * FT + threadIdx.x;
-        if (i >= S.n) break;
-        const uint64_t row = S.begin + i;
-        double u, w;
-        point_u(rp, u1, u2, n_rows, row, scale, u, w);
-        u = clamp_unit(u);
-        w = clamp_unit(w);
-        const unsigned long long p1 = rp[row], p2 = rp[n_rows + row];
-        const PointFull p = eval_point<FAM>(theta, u, w, T64, row, gtab ? gtab + goff[m] : nullptr, p1, p2);
-        zb[row] = p.score;
-        // cross_j to its sorted position (random within the block: L2-resident
-        // while the block's tiles are in flight), run-start flag beside it
-        const uint64_t q1 = S.begin + rank_pos(p1), q2 = n_rows + S.begin + rank_pos(p2);
-        Ag[q1] = p.cross1;
-        Ag[q2] = p.cross2;
-        Fg[q1] = rank_first(p1) ? 1 : 0;
-        Fg[q2] = rank_first(p2) ? 1 : 0;
-        v[0] += p.hess;
-        v[1] += u * p.cross1;
-        v[2] += w * p.cross2;
-        v[3] += clip_log(p.logc);
+    constexpr int U = 2;  // points per thread in flight
+    for (int k0 = 0; k0 < PPT; k0 += U) {
+        unsigned long long p1[U], p2[U];
+        double2 tt[U];
+        double uu[U], ww[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            if (i < S.n) {
+                const uint64_t row = S.begin + i;
+                p1[j] = rp[row];
+                p2[j] = rp[n_rows + row];
+                if (u1) {
+                    uu[j] = u1[row];
+                    ww[j] = u2[row];
+                }
+                if (T64) tt[j] = T64[row];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            if (i >= S.n) continue;
+            const uint64_t row = S.begin + i;
+            double u = u1 ? uu[j] : __dmul_rn(0.5 * static_cast<double>(rank_r2(p1[j])), scale);
+            double w = u1 ? ww[j] : __dmul_rn(0.5 * static_cast<double>(rank_r2(p2[j])), scale);
+            u = clamp_unit(u);
+            w = clamp_unit(w);
+            if (gt) tt[j] = make_double2(gt[rank_r2(p1[j])], gt[rank_r2(p2[j])]);
+            const PointFull p = eval_point<FAM>(th, u, w, tt[j], has_t);
+            zb[row] = p.score;
+            // cross_j to its sorted position (random within the block: L2-resident
+            // while the block's tiles are in flight), run-start flag beside it
+            const uint64_t q1 = S.begin + rank_pos(p1[j]), q2 = n_rows + S.begin + rank_pos(p2[j]);
+            Ag[q1] = with_flag(p.cross1, rank_first(p1[j]));
+            Ag[q2] = with_flag(p.cross2, rank_first(p2[j]));
+            v[0] += p.hess;
+            v[1] += u * p.cross1;
+            v[2] += w * p.cross2;
+            v[3] += clip_log(p.logc);
+        }
     }
     __shared__ double sh[(FT / 32) * 4];
     if (!tile_reduce<4>(v, sh, partials, tickets, S, m, tile)) return;
@@ -123,10 +159,29 @@ __device__ __forceinline__ double finish_sigma2(BlockState& s, double zz, double
 }
 
 // ------------------------------------------------------------ pass 2 (cluster)
+// W_j(row) += value on the row's home CTA (DSMEM reduction; each row gets
+// one store for column 1 and one add for column 2, so the result is exact
+// and order-independent).
+__device__ __forceinline__ void dsmem_add_f64(double* local_slot, uint32_t rank, double v) {
+    const uint32_t la = static_cast<uint32_t>(__cvta_generic_to_shared(local_slot));
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
+    asm volatile("red.relaxed.cluster.shared::cluster.add.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+
 template <int DUMMY>
 __global__ void __launch_bounds__(VT, 1) k_var_w(BlockState* st, const Seg* segs, const int* seg_list,
-                                                const unsigned long long* rp, uint64_t n_rows, double* zb,
-                                                const double* Ag, const uint8_t* Fg, int CL, uint32_t SMAX) {
+                                                const uint32_t* __restrict__ ord, uint64_t n_rows,
+                                                const double* __restrict__ zb, const double* __restrict__ Ag, int CL,
+                                                uint32_t SMAX, unsigned long long* prof) {
+    long long t_prev = clock64();
+    auto mark = [&](int k) {  // optional phase timing (PCB_VAR_PROFILE)
+        if (prof && threadIdx.x == 0) {
+            const long long t = clock64();
+            atomicAdd(prof + k, static_cast<unsigned long long>(t - t_prev));
+            t_prev = t;
+        }
+    };
     cg::cluster_group cluster = cg::this_cluster();
     const int r = static_cast<int>(cluster.block_rank());
     const int m = seg_list[blockIdx.x / CL];
@@ -139,124 +194,110 @@ __global__ void __launch_bounds__(VT, 1) k_var_w(BlockState* st, const Seg* segs
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const double nd = static_cast<double>(n);
 
+    // CTA r owns sorted positions [a, e) AND home rows [a, e) of the block
     extern __shared__ __align__(16) unsigned char smem[];
-    double* A = reinterpret_cast<double*>(smem);             // this CTA's slice of sorted positions
-    uint8_t* flags = reinterpret_cast<uint8_t*>(A + SMAX);  // run-start byte per position
-    __shared__ double s_tot, s_off, s_z;
+    double* A = reinterpret_cast<double*>(smem);               // suffix sums of its positions
+    double* wacc = A + SMAX;                                   // W_1 + W_2 of its home rows
+    uint32_t* bits = reinterpret_cast<uint32_t*>(wacc + SMAX);  // run-start bit per position
+    __shared__ double s_tot, s_z;
     __shared__ double s_red[VNW];
-    __shared__ double s_ch[VNW], s_ch2[VNW];
+    __shared__ double s_wt[VNW], s_wo[VNW];
 
-    double zz = 0.0;
-    constexpr int VU = 4;  // points per thread in flight
+    // warp w owns the contiguous positions [w*WL, (w+1)*WL) of the slice (WL % 32 == 0)
+    const uint32_t WL = ((len + VNW - 1) / VNW + 31) & ~31u;
+    const uint32_t w0 = min(len, wid * WL), w1 = min(len, w0 + WL);
+
     for (int col = 0; col < 2; ++col) {
         const double cj = col ? st[m].c2 : st[m].c1;
-        const unsigned long long* rpc = rp + static_cast<uint64_t>(col) * n_rows + S.begin;
         const double* Aj = Ag + static_cast<uint64_t>(col) * n_rows + S.begin + a;
-        const uint8_t* Fj = Fg + static_cast<uint64_t>(col) * n_rows + S.begin + a;
-        cluster.sync();  // the previous column's gathers from A / flags are done everywhere
-        // this slice of the sorted cross values and run-start flags (contiguous, coalesced)
-        for (uint32_t q0 = tid; q0 < len; q0 += VT * VU) {
-            double c[VU];
-            uint8_t f[VU];
+        const uint32_t* Oj = ord + static_cast<uint64_t>(col) * n_rows + S.begin + a;
+        cluster.sync();  // the previous column's walks over A / bits are done everywhere
+        mark(0);
+        // load this warp's positions (coalesced), peel the run-start bits, warp total
+        double wsum = 0.0;
+        for (uint32_t q0 = w0; q0 < w1; q0 += 32 * 4) {
+            double c[4];
 #pragma unroll
-            for (int u = 0; u < VU; ++u) {
-                const uint32_t q = q0 + u * VT;
-                if (q < len) {
-                    c[u] = Aj[q];
-                    f[u] = Fj[q];
-                }
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t q = q0 + u * 32 + lane;
+                c[u] = q < w1 ? Aj[q] : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < VU; ++u) {
-                const uint32_t q = q0 + u * VT;
-                if (q < len) {
-                    A[q] = c[u];
-                    flags[q] = f[u];
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t q = q0 + u * 32 + lane;
+                const unsigned fb = __ballot_sync(0xffffffffu, q < w1 && flag_of(c[u]));
+                if (q0 + u * 32 < w1) {
+                    if (lane == 0) bits[(q0 + u * 32) >> 5] = fb;
+                    if (q < w1) A[q] = c[u];
+                    wsum += c[u];
                 }
             }
         }
+        wsum = warp_sum(wsum);
+        if (lane == 0) s_wt[wid] = wsum;
         __syncthreads();
-        // suffix sums of this slice: slice total first, then a reverse tiled scan
-        double tv[1] = {0.0};
-        for (uint32_t q = tid; q < len; q += VT) tv[0] += A[q];
-        block_sum<1>(tv, s_red);
-        if (tid == 0) s_tot = tv[0];
-        cluster.sync();  // slice totals published
-        if (tid == 0) {
-            double off = 0.0;
-            for (int q = r + 1; q < CL; ++q) off += *cluster.map_shared_rank(&s_tot, q);
-            s_off = off;
-        }
-        __syncthreads();
-        double carry = s_off;
-        const uint32_t ntile = (len + VT - 1) / VT;
-        for (uint32_t t = ntile; t-- > 0;) {
-            const uint32_t q = t * VT + tid;
-            const double v = q < len ? A[q] : 0.0;
-            double x = v;  // inclusive suffix within the warp
+        if (wid == 0) {  // exclusive suffix of the warp totals; slice total
+            double x = s_wt[lane];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const double y = __shfl_down_sync(0xffffffffu, x, o);
                 if (lane + o < 32) x += y;
             }
-            if (lane == 0) s_ch[wid] = x;
-            __syncthreads();
-            if (wid == 0) {  // inclusive suffix over the warp totals (fixed order)
-                double y = s_ch[lane];
+            s_wo[lane] = x - s_wt[lane];
+            if (lane == 0) s_tot = x;
+        }
+        mark(1);
+        cluster.sync();  // slice totals published
+        double carry = s_wo[wid];
+        for (int q = r + 1; q < CL; ++q) carry += *cluster.map_shared_rank(&s_tot, q);  // slices above
+        // suffix scan of the warp's positions, top tile first
+        for (uint32_t t = (w1 - w0 + 31) / 32; t-- > 0;) {
+            const uint32_t q = w0 + t * 32 + lane;
+            double x = q < w1 ? A[q] : 0.0;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const double z2 = __shfl_down_sync(0xffffffffu, y, o);
-                    if (lane + o < 32) y += z2;
-                }
-                s_ch2[lane] = y;
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_down_sync(0xffffffffu, x, o);
+                if (lane + o < 32) x += y;
             }
-            __syncthreads();
-            const double later = wid + 1 < VNW ? s_ch2[wid + 1] : 0.0;  // warps above this one
-            if (q < len) A[q] = carry + later + x;
-            carry += s_ch2[0];
-            __syncthreads();
+            if (q < w1) A[q] = carry + x;
+            carry += __shfl_sync(0xffffffffu, x, 0);
         }
         cluster.sync();  // suffix sums complete everywhere
-        // gather T_j at each point's run start
-        for (uint32_t i0 = a + tid; i0 < e; i0 += VT * VU) {
-            unsigned long long p[VU];
-            double zv[VU];
-#pragma unroll
-            for (int u = 0; u < VU; ++u) {
-                const uint32_t i = i0 + u * VT;
-                if (i < e) {
-                    p[u] = rpc[i];
-                    zv[u] = zb[S.begin + i];
-                }
-            }
-            double tj[VU];
-#pragma unroll
-            for (int u = 0; u < VU; ++u) {
-                if (i0 + u * VT < e) {
-                    uint32_t q = rank_pos(p[u]);
-                    if (!rank_first(p[u])) {  // tied, not first: nearest run start below q
-                        do {
-                            --q;  // position 0 always starts a run
-                        } while (!*cluster.map_shared_rank(flags + (q - (q / SL) * SL), q / SL));
+        mark(2);
+        // W_j of the row at each of this CTA's positions -> pushed to the row's home CTA
+        for (uint32_t p = tid; p < len; p += VT) {
+            const uint32_t row = Oj[p];
+            double T;
+            if ((bits[p >> 5] >> (p & 31)) & 1u) {
+                T = A[p];
+            } else {  // tied, not first: highest run-start bit below this position
+                uint32_t t = a + p - 1;
+                uint32_t q;
+                for (;;) {
+                    const uint32_t o = t / SL, lt = t - o * SL;
+                    uint32_t w = *cluster.map_shared_rank(bits + (lt >> 5), o);
+                    w &= 0xffffffffu >> (31 - (lt & 31));
+                    if (w) {
+                        q = o * SL + (lt & ~31u) + (31 - __clz(w));
+                        break;
                     }
-                    const uint32_t o = q / SL;
-                    tj[u] = *cluster.map_shared_rank(A + (q - o * SL), o);
+                    t = o * SL + (lt & ~31u) - 1;  // position 0 always starts a run
                 }
+                const uint32_t o = q / SL;
+                T = *cluster.map_shared_rank(A + (q - o * SL), o);
             }
-#pragma unroll
-            for (int u = 0; u < VU; ++u) {
-                const uint32_t i = i0 + u * VT;
-                if (i < e) {
-                    const double wj = (tj[u] - cj) / nd;
-                    if (col == 0) {
-                        zb[S.begin + i] = zv[u] + wj;  // score + W_1
-                    } else {
-                        const double z = zv[u] + wj;
-                        zz += z * z;
-                    }
-                }
-            }
+            const double wj = (T - cj) / nd;
+            const uint32_t h = row / SL, slot = row - h * SL;
+            if (col == 0) *cluster.map_shared_rank(wacc + slot, h) = wj;
+            else dsmem_add_f64(wacc + slot, h, wj);
         }
+        mark(3);
+    }
+    cluster.sync();  // every W has reached its home row
+    double zz = 0.0;
+    for (uint32_t i = tid; i < len; i += VT) {
+        const double z = zb[S.begin + a + i] + wacc[i];
+        zz += z * z;
     }
     // fixed-order reduction of sum z^2: block, then cluster
     double v[1] = {zz};
@@ -270,8 +311,6 @@ __global__ void __launch_bounds__(VT, 1) k_var_w(BlockState* st, const Seg* segs
         s.sigma2 = finish_sigma2(s, tot, nd);
         st[m] = s;
     }
-    (void)lane;
-    (void)wid;
     cluster.sync();  // peers' shared memory is read above
 }
 
@@ -302,15 +341,15 @@ __global__ void __launch_bounds__(1024) k_suffix_g(const BlockState* st, const S
     }
     double run = threadIdx.x + 1 < blockDim.x ? s_tot[threadIdx.x + 1] : 0.0;
     for (uint32_t q = b1; q-- > b0;) {
-        run += a[q];
-        a[q] = run;
+        const double x = a[q];
+        run += x;
+        a[q] = with_flag(run, flag_of(x));  // the run-start flag stays with its position
     }
 }
 
 __global__ void __launch_bounds__(FT) k_var_gather_g(BlockState* st, const Seg* segs, int nseg, const uint8_t* use,
                                                     const unsigned long long* rp, uint64_t n_rows, const double* zb,
-                                                    const double* A, const uint8_t* F, double* partials,
-                                                    unsigned* tickets) {
+                                                    const double* A, double* partials, unsigned* tickets) {
     const uint32_t tile = blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
@@ -331,7 +370,7 @@ __global__ void __launch_bounds__(FT) k_var_gather_g(BlockState* st, const Seg* 
             if (!rank_first(p))
                 do {
                     --q;  // position 0 always starts a run
-                } while (!F[b0 + q]);
+                } while (!flag_of(A[b0 + q]));
             z += (A[b0 + q] - cjs[col]) / nd;
         }
         v[0] += z * z;
@@ -362,22 +401,22 @@ VarPlan plan_var(uint64_t nmax) {
         p.cl = cl;
         p.smax = static_cast<uint32_t>((nmax + cl - 1) / cl);
         p.smax = (p.smax + 31u) & ~31u;
-        p.smem = static_cast<size_t>(p.smax) * 9;
+        p.smem = static_cast<size_t>(p.smax) * 16 + (p.smax / 32 + 1) * 4;
         if (p.smem <= kVarSmem) return p;
     }
     return VarPlan{};
 }
 
 template <int FAM>
-void launch_var_point(Ctx& c, const VarIO& v, double* zb, double* Ag, uint8_t* Fg) {
+void launch_var_point(Ctx& c, const VarIO& v, double* zb, double* Ag) {
     const int K = static_cast<int>(v.off->size() - 1);
     k_var_point<FAM><<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, v.rp, v.u1, v.u2, v.T64, v.gtab, v.goff,
-                                                   v.n_rows, zb, Ag, Fg, v.partials, v.tickets);
+                                                   v.n_rows, zb, Ag, v.partials, v.tickets);
     c.count_launch();
 }
 
 void launch_var_w(Ctx& c, const VarPlan& p, const VarIO& v, const int* seg_list, int njobs, double* zb,
-                  const double* Ag, const uint8_t* Fg) {
+                  const double* Ag) {
     auto k = k_var_w<0>;
     PCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)));
     if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -393,14 +432,28 @@ void launch_var_w(Ctx& c, const VarPlan& p, const VarIO& v, const int* seg_list,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    PCB_CUDA(cudaLaunchKernelEx(&cfg, k, v.st, v.segs, seg_list, v.rp, v.n_rows, zb, Ag, Fg, p.cl, p.smax));
+    unsigned long long* prof = nullptr;
+    const char* pe = std::getenv("PCB_VAR_PROFILE");
+    if (pe && pe[0] == '1') {
+        prof = c.ws.get_t<unsigned long long>("var.prof", 8);
+        PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
+    }
+    PCB_CUDA(cudaLaunchKernelEx(&cfg, k, v.st, v.segs, seg_list, v.ord, v.n_rows, zb, Ag, p.cl, p.smax, prof));
     c.count_launch();
+    if (prof) {
+        unsigned long long h[8];
+        PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+        const double ctas = static_cast<double>(njobs) * p.cl;
+        std::fprintf(stderr, "[var profile] CL=%d smax=%u cycles/CTA (both columns): sync %.0f  load %.0f  scan %.0f  gather %.0f\n",
+                     p.cl, p.smax, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas);
+    }
 }
 
-void launch_var_global(Ctx& c, const VarIO& v, const uint8_t* use, double* zb, double* Ag, const uint8_t* Fg) {
+void launch_var_global(Ctx& c, const VarIO& v, const uint8_t* use, double* zb, double* Ag) {
     const int K = static_cast<int>(v.off->size() - 1);
     k_suffix_g<<<2 * K, 1024, 0, c.stream>>>(v.st, v.segs, K, use, v.n_rows, Ag);
-    k_var_gather_g<<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, use, v.rp, v.n_rows, zb, Ag, Fg, v.partials,
+    k_var_gather_g<<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, use, v.rp, v.n_rows, zb, Ag, v.partials,
                                                  v.tickets);
     c.count_launch(2);
 }
@@ -412,10 +465,11 @@ void run_variance(Ctx& c, const VarIO& v) {
     const int K = static_cast<int>(off.size() - 1);
     auto* zb = c.ws.get_t<double>("var.z", v.n_rows);
     auto* Ag = c.ws.get_t<double>("var.A", 2 * v.n_rows);
-    auto* Fg = c.ws.get_t<uint8_t>("var.F", 2 * v.n_rows);
-    if (v.family == kGaussian) launch_var_point<kGaussian>(c, v, zb, Ag, Fg);
-    else if (v.family == kFrank) launch_var_point<kFrank>(c, v, zb, Ag, Fg);
-    else launch_var_point<kGumbel>(c, v, zb, Ag, Fg);
+    PCB_CUDA(cudaEventRecord(c.ev[6], c.stream));
+    if (v.family == kGaussian) launch_var_point<kGaussian>(c, v, zb, Ag);
+    else if (v.family == kFrank) launch_var_point<kFrank>(c, v, zb, Ag);
+    else launch_var_point<kGumbel>(c, v, zb, Ag);
+    PCB_CUDA(cudaEventRecord(c.ev[7], c.stream));
     uint64_t nmax = 0;
     for (int m = 0; m < K; ++m) nmax = std::max<uint64_t>(nmax, off[m + 1] - off[m]);
     const VarPlan p = plan_var(nmax);
@@ -424,13 +478,17 @@ void run_variance(Ctx& c, const VarIO& v) {
         for (int m = 0; m < K; ++m) jobs[m] = m;
         int* d_jobs = c.ws.get_t<int>("var.jobs", K);
         PCB_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), K * sizeof(int), cudaMemcpyHostToDevice, c.stream));
-        launch_var_w(c, p, v, d_jobs, K, zb, Ag, Fg);
+        launch_var_w(c, p, v, d_jobs, K, zb, Ag);
     } else {
         std::vector<uint8_t> use(K, 1);
         uint8_t* d_use = c.ws.get_t<uint8_t>("var.use", K);
         PCB_CUDA(cudaMemcpyAsync(d_use, use.data(), K, cudaMemcpyHostToDevice, c.stream));
-        launch_var_global(c, v, d_use, zb, Ag, Fg);
+        launch_var_global(c, v, d_use, zb, Ag);
     }
+    PCB_CUDA(cudaEventSynchronize(c.ev[7]));
+    float ms = 0.0f;
+    PCB_CUDA(cudaEventElapsedTime(&ms, c.ev[6], c.ev[7]));
+    c.stage_ms[9] = ms;  // variance pass 1 (per-point terms); the rest of [3] is pass 2
 }
 
 }  // namespace pcb

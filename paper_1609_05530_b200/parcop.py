@@ -175,7 +175,7 @@ class Context:
         buf = (C.c_double * 12)()
         k = self.lib.pcb_stage_times(self.ptr, buf, 12)
         names = ["rank", "prepare", "newton", "variance", "finalize", "lik_kernel_ms", "lik_launches",
-                 "warm_kernel_ms", "warm_launches"]
+                 "warm_kernel_ms", "warm_launches", "var_point_ms"]
         return {names[i]: float(buf[i]) for i in range(k)}
 
     def trim(self):
