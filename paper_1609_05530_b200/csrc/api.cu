@@ -4,6 +4,7 @@
 // device or fails with PCB_E_CUDA.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -175,6 +176,52 @@ void pipeline_blocks(pcb::Ctx& c, int fam, int prec, const double* d1, const dou
     finish_stage_times(c);
 }
 
+// Host-resident inputs: stream the columns block-group by block-group on a
+// copy stream into two device buffers, so the H2D of group g+1 overlaps the
+// rank/fit/variance of group g. Groups are whole blocks, so every block's
+// result is the same as in one call (bitwise).
+void pipeline_blocks_host(pcb::Ctx& c, int fam, int prec, const double* h1, const double* h2, uint64_t n_rows,
+                          const std::vector<uint64_t>& off, pcb_fit_result* d_out) {
+    const uint64_t K = off.size() - 1;
+    uint64_t target = 1ull << 26;  // rows per group (512 MB per column)
+    if (const char* v = std::getenv("PCB_STREAM_ROWS")) target = std::max<uint64_t>(1024, std::strtoull(v, nullptr, 10));
+    std::vector<std::pair<uint64_t, uint64_t>> groups;
+    for (uint64_t b0 = 0; b0 < K;) {
+        uint64_t b1 = b0 + 1;
+        while (b1 < K && off[b1 + 1] - off[b0] <= target) ++b1;
+        groups.push_back({b0, b1});
+        b0 = b1;
+    }
+    if (groups.size() == 1) {
+        const double* d1 = dev_in(c, h1, n_rows, "c1");
+        const double* d2 = dev_in(c, h2, n_rows, "c2");
+        pipeline_blocks(c, fam, prec, d1, d2, n_rows, off, d_out);
+        return;
+    }
+    uint64_t maxrows = 0;
+    for (auto& g : groups) maxrows = std::max(maxrows, off[g.second] - off[g.first]);
+    double* buf[2][2];
+    for (int b = 0; b < 2; ++b)
+        for (int j = 0; j < 2; ++j)
+            buf[b][j] = c.ws.get_t<double>(std::string("strm.") + char('0' + b) + char('0' + j), maxrows);
+    auto enqueue = [&](size_t g) {
+        const uint64_t r0 = off[groups[g].first], rows = off[groups[g].second] - r0;
+        double** d = buf[g & 1];
+        PCB_CUDA(cudaMemcpyAsync(d[0], h1 + r0, rows * sizeof(double), cudaMemcpyHostToDevice, c.copy_stream));
+        PCB_CUDA(cudaMemcpyAsync(d[1], h2 + r0, rows * sizeof(double), cudaMemcpyHostToDevice, c.copy_stream));
+        PCB_CUDA(cudaEventRecord(c.cev[g & 1], c.copy_stream));
+    };
+    enqueue(0);
+    for (size_t g = 0; g < groups.size(); ++g) {
+        if (g + 1 < groups.size()) enqueue(g + 1);  // its buffer's previous user (group g-1) has finished
+        PCB_CUDA(cudaStreamWaitEvent(c.stream, c.cev[g & 1], 0));
+        const uint64_t b0 = groups[g].first, b1 = groups[g].second, r0 = off[b0];
+        std::vector<uint64_t> og(b1 - b0 + 1);
+        for (uint64_t b = b0; b <= b1; ++b) og[b - b0] = off[b] - r0;
+        pipeline_blocks(c, fam, prec, buf[g & 1][0], buf[g & 1][1], off[b1] - r0, og, d_out + b0);
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -206,6 +253,8 @@ pcb_context* pcb_create(int device) {
         PCB_CUDA(cudaStreamCreateWithFlags(&ctx->c.own_stream, cudaStreamNonBlocking));
         ctx->c.stream = ctx->c.own_stream;
         for (auto& ev : ctx->c.ev) PCB_CUDA(cudaEventCreate(&ev));
+        for (auto& ev : ctx->c.cev) PCB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        PCB_CUDA(cudaStreamCreateWithFlags(&ctx->c.copy_stream, cudaStreamNonBlocking));
         pcb::init_tables();
         return ctx;
     } catch (const std::exception& ex) {
@@ -221,6 +270,12 @@ void pcb_destroy(pcb_context* ctx) {
     ctx->c.ws.release();
     for (auto& ev : ctx->c.ev)
         if (ev) cudaEventDestroy(ev);
+    for (auto& ev : ctx->c.cev)
+        if (ev) cudaEventDestroy(ev);
+    if (ctx->c.copy_stream) {
+        cudaStreamSynchronize(ctx->c.copy_stream);
+        cudaStreamDestroy(ctx->c.copy_stream);
+    }
     if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
     delete ctx;
@@ -441,10 +496,14 @@ int pcb_fit_blocks(pcb_context* ctx, int family, int precision, const double* co
         check_precision(precision);
         if (!col1 || !col2 || !out) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
         const auto off = check_offsets(seg_offsets, n_seg, n_rows, 2);
-        const double* d1 = dev_in(c, col1, n_rows, "c1");
-        const double* d2 = dev_in(c, col2, n_rows, "c2");
         DevOut<pcb_fit_result> o(c, out, n_seg, "fit");
-        pipeline_blocks(c, family, precision, d1, d2, n_rows, off, o.dev);
+        if (!is_device_ptr(col1) && !is_device_ptr(col2)) {
+            pipeline_blocks_host(c, family, precision, col1, col2, n_rows, off, o.dev);
+        } else {
+            const double* d1 = dev_in(c, col1, n_rows, "c1");
+            const double* d2 = dev_in(c, col2, n_rows, "c2");
+            pipeline_blocks(c, family, precision, d1, d2, n_rows, off, o.dev);
+        }
         o.finish(c);
         PCB_CUDA(cudaStreamSynchronize(c.stream));
     });
@@ -463,9 +522,17 @@ int pcb_fit_parallel(pcb_context* ctx, int family, int precision, const double* 
         if (n_blocks < 1) throw pcb::Error(PCB_E_INVALID, "partition: need M >= 1");
         if (pcb_partition(n_rows, n_blocks, scheme, off.data()) != PCB_OK)
             throw pcb::Error(PCB_E_INVALID, "partition: block below the 30-row floor");
-        const double* d1 = dev_in(c, col1, n_rows, "c1");
-        const double* d2 = dev_in(c, col2, n_rows, "c2");
-        if (scheme == PCB_STRIDED) {
+        auto* rec = c.ws.get_t<pcb_fit_result>("par.rec", n_blocks);
+        const bool host_in = !is_device_ptr(col1) && !is_device_ptr(col2);
+        const double* d1 = nullptr;
+        const double* d2 = nullptr;
+        if (scheme == PCB_CONTIGUOUS && host_in) {
+            pipeline_blocks_host(c, family, precision, col1, col2, n_rows, off, rec);
+        } else {
+            d1 = dev_in(c, col1, n_rows, "c1");
+            d2 = dev_in(c, col2, n_rows, "c2");
+        }
+        if (d1 && scheme == PCB_STRIDED) {
             double* g1 = c.ws.get_t<double>("strided.c1", n_rows);
             double* g2 = c.ws.get_t<double>("strided.c2", n_rows);
             pcb::run_strided_gather(c, d1, n_rows, n_blocks, g1);
@@ -473,8 +540,7 @@ int pcb_fit_parallel(pcb_context* ctx, int family, int precision, const double* 
             d1 = g1;
             d2 = g2;
         }
-        auto* rec = c.ws.get_t<pcb_fit_result>("par.rec", n_blocks);
-        pipeline_blocks(c, family, precision, d1, d2, n_rows, off, rec);
+        if (d1) pipeline_blocks(c, family, precision, d1, d2, n_rows, off, rec);
         DevOut<double> w(c, weights, weights ? n_blocks : 0, "w");
         double* d3 = c.ws.get_t<double>("comb.out", 3);
         pcb::run_combine(c, rec, n_blocks, weights ? w.dev : nullptr, d3);

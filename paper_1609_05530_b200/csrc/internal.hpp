@@ -68,6 +68,8 @@ struct Ctx {
     double stage_ms[12] = {0};
     int n_stage = 0;
     cudaEvent_t ev[8] = {};
+    cudaStream_t copy_stream = nullptr;  // host->device streaming of inputs (overlaps compute)
+    cudaEvent_t cev[4] = {};
     // pinned host staging for small results
     void* pinned = nullptr;
     size_t pinned_bytes = 0;

@@ -409,8 +409,8 @@ inline ClusterPlan plan_cluster(uint64_t nmax) {
 }
 
 __device__ __forceinline__ uint32_t cbucket(unsigned long long k, double hm, double scale, uint32_t nbtot) {
-    const double t = (0.5 * key_value(k) - hm) * scale;
-    return t < static_cast<double>(nbtot) ? static_cast<uint32_t>(t) : nbtot - 1u;
+    const double t = (0.5 * key_value(k) - hm) * scale;  // monotone in k; clamped at both ends
+    return t > 0.0 ? (t < static_cast<double>(nbtot) ? static_cast<uint32_t>(t) : nbtot - 1u) : 0u;
 }
 
 // Same scan over NBL u16 counters packed two per word (`cw`); writes the u16
@@ -492,65 +492,76 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     __shared__ uint32_t s_off[kMaxCluster], s_total, s_base;
     __shared__ uint32_t s_w[NWARP];
 
-    // ---- 1. slice extremes (all EMAX loads of a thread in flight together)
+    // ---- 1. bucket-map range from a strided sample (one element per thread).
+    // Any monotone map gives exact ranks (values outside the sampled range
+    // clamp into the end buckets); the range only sets the load balance. A
+    // constant-looking sample triggers an exact pass (constant columns).
     unsigned long long kmn = ~0ull, kmx = 0ull;
-    bool fin = true;
+    const uint32_t len = e - a;
+    if (len > 0) {
+        const unsigned long long kk = order_key(x[a + static_cast<uint32_t>((static_cast<uint64_t>(tid) * len) / CT)]);
+        kmn = kk;
+        kmx = kk;
+    }
+    auto cta_extremes = [&]() {
 #pragma unroll
-    for (int k = 0; k < EMAX; ++k) {
-        const uint32_t i = a + k * CT + tid;
-        if (i < e) {
-            const double v = x[i];
-            fin &= isfinite(v);
-            const unsigned long long kk = order_key(v);
+        for (int o = 16; o > 0; o >>= 1) {
+            kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+            kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+        }
+        if (lane == 0) {
+            s_k[0][wid] = kmn;
+            s_k[1][wid] = kmx;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < NWARP; ++w) {
+                kmn = min(kmn, s_k[0][w]);
+                kmx = max(kmx, s_k[1][w]);
+            }
+            s_rmin = kmn;
+            s_rmax = kmx;
+        }
+    };
+    auto cluster_extremes = [&]() {
+        if (tid == 0) {
+            unsigned long long gmn = ~0ull, gmx = 0ull;
+            for (int q = 0; q < CL; ++q) {
+                gmn = min(gmn, *cluster.map_shared_rank(&s_rmin, q));
+                gmx = max(gmx, *cluster.map_shared_rank(&s_rmax, q));
+            }
+            s_gmin = gmn;
+            s_gmax = gmx;
+        }
+        __syncthreads();
+    };
+    if (tid == 0) s_bad = 0;
+    for (int q = tid; q < NWARP * kMaxCluster; q += CT) (&s_wc[0][0])[q] = 0u;
+    cta_extremes();
+    cluster.sync();
+    mark(0);
+    cluster_extremes();
+    if (s_gmin == s_gmax) {  // exact extremes over every element (all CTAs agree on taking this branch)
+        kmn = ~0ull;
+        kmx = 0ull;
+        for (uint32_t i = a + tid; i < e; i += CT) {
+            const unsigned long long kk = order_key(x[i]);
             kmn = min(kmn, kk);
             kmx = max(kmx, kk);
         }
+        __syncthreads();
+        cluster.sync();  // everyone has read the sample extremes
+        cta_extremes();
+        cluster.sync();
+        cluster_extremes();
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
-        kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
-    }
-    fin = __all_sync(0xffffffffu, fin);
-    if (tid == 0) s_bad = 0;
-    for (int q = tid; q < NWARP * kMaxCluster; q += CT) (&s_wc[0][0])[q] = 0u;
-    __syncthreads();
-    if (lane == 0) {
-        s_k[0][wid] = kmn;
-        s_k[1][wid] = kmx;
-        if (!fin) s_bad = 1;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        for (int w = 1; w < NWARP; ++w) {
-            kmn = min(kmn, s_k[0][w]);
-            kmx = max(kmx, s_k[1][w]);
-        }
-        s_rmin = kmn;
-        s_rmax = kmx;
-    }
-    cluster.sync();
-    mark(0);
-    if (tid == 0) {
-        unsigned long long gmn = ~0ull, gmx = 0ull;
-        int gb = 0;
-        for (int q = 0; q < CL; ++q) {
-            gmn = min(gmn, *cluster.map_shared_rank(&s_rmin, q));
-            gmx = max(gmx, *cluster.map_shared_rank(&s_rmax, q));
-            gb |= *cluster.map_shared_rank(&s_bad, q);
-        }
-        s_gmin = gmn;
-        s_gmax = gmx;
-        s_gbad = gb;
-    }
-    __syncthreads();
     const double vmin = key_value(s_gmin), vmax = key_value(s_gmax);
     const double hm = 0.5 * vmin;
     const uint32_t nbtot = static_cast<uint32_t>(CL) << lg_nbl;
     const double scale = static_cast<double>(nbtot) / (0.5 * vmax - hm);
     const bool constant = s_gmin == s_gmax;
-    if (s_gbad || constant || !(isfinite(scale) && scale > 0.0 && isfinite(hm))) {
-        if (s_gbad) {
+    if (constant || !(isfinite(scale) && scale > 0.0 && isfinite(hm))) {
+        if (constant && !isfinite(vmin)) {
             if (r == 0 && tid == 0) bad[J.seg] = 1;
         } else if (constant) {  // one tie run: avg rank (n+1)/2 for all, stable positions = row order
             for (uint32_t i = a + tid; i < e; i += CT) {
@@ -569,16 +580,19 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     uint32_t bk[(EMAX + 1) / 2];
 #pragma unroll
     for (int k = 0; k < (EMAX + 1) / 2; ++k) bk[k] = 0u;
+    bool fin = true;
 #pragma unroll
     for (int k = 0; k < EMAX; ++k) {
         const uint32_t i = a + k * CT + tid;
         if (i < e) {
-            const uint32_t b = cbucket(order_key(x[i]), hm, scale, nbtot);
+            const double v = x[i];
+            fin &= isfinite(v);
+            const uint32_t b = cbucket(order_key(v), hm, scale, nbtot);
             bk[k >> 1] |= b << ((k & 1) * 16);
             atomicAdd(&s_wc[wid][b >> lg_nbl], 1u);
         }
     }
-    __syncthreads();
+    if (!__syncthreads_and(fin) && tid == 0) s_bad = 1;  // validate_data (pseudo_obs.hpp:34-36)
     if (tid < CL) {  // totals per owner, and per-warp exclusive bases
         uint32_t run = 0;
         for (int w = 0; w < NWARP; ++w) {
@@ -591,7 +605,17 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     cluster.sync();
     mark(1);
     if (tid < CL * CL) s_mat[tid] = *cluster.map_shared_rank(&s_cnt[tid % CL], tid / CL);  // [src][dst]
+    if (tid == 0) {
+        int gb = 0;
+        for (int q = 0; q < CL; ++q) gb |= *cluster.map_shared_rank(&s_bad, q);
+        s_gbad = gb;
+    }
     __syncthreads();
+    if (s_gbad) {
+        if (r == 0 && tid == 0) bad[J.seg] = 1;
+        cluster.sync();
+        return;
+    }
     if (tid == 0) {
         int over = 0;
         uint32_t base = 0, total = 0;
@@ -658,7 +682,11 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     // ---- 5. rank inside each bucket; write packed (r2 | pos | run-start)
     unsigned long long* out = rp + static_cast<uint64_t>(J.col) * n_rows + J.begin;
     uint32_t* ordo = ord + static_cast<uint64_t>(J.col) * n_rows + J.begin;
-    for (uint32_t j = tid; j < T; j += CT) {
+    // walk the elements in bucket order: a warp's lanes mostly share buckets, so
+    // the bucket-mate loads are shared-memory broadcasts and the order writes
+    // are nearly contiguous
+    for (uint32_t qq = tid; qq < T; qq += CT) {
+        const uint32_t j = perm[qq];
         const unsigned long long k = recv_key[j];
         const uint32_t id = recv_idx[j];  // (local bucket << kIdxBits) | row: same bucket => compares as row
         const uint32_t lb = id >> kIdxBits;

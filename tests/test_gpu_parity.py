@@ -312,3 +312,19 @@ def test_variance_large_segment_global(ctx, orc):
     got = pcb.fit_blocks(2, X, [0, n], ctx=ctx)
     want = orc.fit_blocks(2, X.col1, X.col2, [0, n])
     check_records(got, want, TOL64)
+
+
+def test_host_streaming_identical(ctx, env):
+    """Host-resident columns are streamed group by group (H2D overlapping
+    compute); every block's record must equal the device-resident call's."""
+    n, k = 64000, 16
+    X = pcb.sample_matrix(2, 2.0, n, k, ctx=ctx)
+    off = pcb.partition(n, k).offsets
+    env.setenv("PCB_STREAM_ROWS", "9000")  # groups of 2 blocks
+    host = pcb.fit_blocks(2, X, off, ctx=ctx)
+    import torch
+    dev = pcb.DataMatrix(torch.from_numpy(X.col1).cuda(), torch.from_numpy(X.col2).cuda())
+    devr = pcb.fit_blocks(2, dev, off, ctx=ctx)
+    assert [(r.theta_hat, r.sigma2, r.loglik) for r in host] == [(r.theta_hat, r.sigma2, r.loglik) for r in devr]
+    res = pcb.fit_parallel(2, X, k, ctx=ctx)
+    assert res.theta_combined == pcb.combine(devr, ctx=ctx).theta_combined
