@@ -40,6 +40,7 @@ BASE_SEED = 0x160905530
 METRIC = "copula fit throughput (points/sec, fp64) at n=1e9, 1/2/4/8 B200, % roofline"
 # SURVEY.md §8(d) frozen algorithmic FP64 instructions per point per theta candidate (F_fit)
 F_FIT = {"gaussian": 9, "frank": 175, "gumbel": 210}
+F_VAR = {"gaussian": 24, "frank": 260, "gumbel": 350}  # per point at theta-hat (variance pass)
 B_PASS = 16  # bytes per point per likelihood pass (fp64 pair)
 
 
@@ -276,23 +277,67 @@ def run_ours(args):
             wms = sa.get("warm_kernel_ms", 0.0) / steps
             entry["warm_fp32"] = {"ms": wms, "launches": wl, "hbm_gbs": 8 * rows * wl / (wms * 1e-3) / 1e9}
         kernels[name] = entry
-    dom = max((k for k in kernels if "lik" in kernels[k]), key=lambda k: kernels[k]["lik"]["ms"], default=None)
+    # ---- roofline: every kernel's share of the step, the dominant one reported
+    # (algorithmic bytes / FP64 instructions per launch)
+    hbm_peak = 6547.2e9  # MEASURED_PEAKS.json hbm_gbs (burst copy)
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]) * 1e9
+    except Exception:
+        pass
+    traffic_db = {}
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic_db = json.load(open(tp))
+        except Exception:
+            traffic_db = {}
+    per_kernel = {}  # name -> [ms, launches, bytes, fp64 instr]
+    def add(name, ms, launches, nbytes, instr):
+        e = per_kernel.setdefault(name, [0.0, 0, 0.0, 0.0])
+        e[0] += ms
+        e[1] += launches
+        e[2] += nbytes
+        e[3] += instr
+    for name, fam, th in FAMILIES:
+        st_ = kernels[name]["stage_ms"]
+        add("k_rank_cluster", st_.get("rank", 0.0), 1, 32.0 * rows, 0.0)
+        # prepare: read 2 packed ranks; write T (f64 pair) + its fp32 warm-up copy (Archimedean)
+        add("k_prepare", st_.get("prepare", 0.0), 1, (16.0 if name == "gaussian" else 40.0) * rows, 0.0)
+        vp = st_.get("var_point_ms", 0.0)
+        # variance pass 1: read ranks (+T for Gumbel); write score + two sorted cross values
+        add("k_var_point", vp, 1, (56.0 if name == "gumbel" else 40.0) * rows, F_VAR[name] * rows)
+        add("k_var_w", st_.get("variance", 0.0) - vp, 1, 32.0 * rows, 0.0)
+        if "lik" in kernels[name]:
+            lk = kernels[name]["lik"]
+            add("k_lik(fp64)", lk["ms"], lk["launches"], B_PASS * rows * lk["fp64_passes"],
+                F_FIT[name] * rows * lk["fp64_passes"])
+        if "warm_fp32" in kernels[name]:
+            wk = kernels[name]["warm_fp32"]
+            add("k_lik(fp32 warm-up)", wk["ms"], wk["launches"], 8.0 * rows * wk["launches"], 0.0)
+    table = {}
+    for kname, (kms, nl, nbytes, instr) in per_kernel.items():
+        if kms <= 0:
+            continue
+        t_hbm, t_fp64 = nbytes / hbm_peak, instr / fp64_peak
+        bound = "fp64" if t_fp64 > t_hbm else "hbm"
+        if bound == "hbm":
+            ach, peak, unit = nbytes / (kms * 1e-3) / 1e9, hbm_peak / 1e9, "GB/s"
+        else:
+            ach, peak, unit = instr / (kms * 1e-3) / 1e12, fp64_peak / 1e12, "T FP64-instr/s"
+        table[kname] = {"ms_per_step": kms, "share": kms / ms, "launches": nl, "bound": bound, "achieved": ach,
+                        "peak": peak, "unit": unit, "frac": ach / peak, "avg_launch_ms": kms / max(nl, 1)}
+    dom = max(table, key=lambda k: table[k]["ms_per_step"]) if table else None
     roof = None
     if dom:
-        lk = kernels[dom]["lik"]
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "lik_traffic.json")
-        if os.path.exists(tp):
-            try:
-                traffic = json.load(open(tp)).get(dom)
-            except Exception:
-                traffic = None
-        roof = {"bound": "fp64", "kernel": f"k_lik<{dom}, double2>", "achieved": lk["fp64_instr_per_s"] / 1e12,
-                "peak": fp64_peak / 1e12, "unit": "T FP64-instr/s", "frac": lk["fp64_instr_per_s"] / fp64_peak,
-                "peak_source": "measured live: DFMA-loop microbenchmark (pcb_measure_fp64_peak)",
-                "traffic": traffic, "algorithmic_per_point": F_FIT[dom],
-                "hbm_frac": lk["hbm_gbs"] / 6547.2}
-
+        tk = table[dom]
+        roof = {"bound": tk["bound"], "kernel": dom, "achieved": tk["achieved"], "peak": tk["peak"], "unit": tk["unit"],
+                "frac": tk["frac"], "share_of_step": tk["share"],
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured)" if tk["bound"] == "hbm"
+                                else "measured live: DFMA-loop microbenchmark (pcb_measure_fp64_peak)"),
+                "traffic": (traffic_db[dom] * rows if dom in traffic_db else None),
+                "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/r01_ncu_full.md, per point x points)",
+                "algorithmic_bytes_per_launch": per_kernel[dom][2] / max(per_kernel[dom][1], 1),
+                "per_kernel": table}
     # ------------------------------------------------------------ e2e
     e2e = None
     if not args.no_e2e:
