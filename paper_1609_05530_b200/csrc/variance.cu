@@ -265,8 +265,19 @@ __global__ void __launch_bounds__(VT, 1) k_var_w(BlockState* st, const Seg* segs
         cluster.sync();  // suffix sums complete everywhere
         mark(2);
         // W_j of the row at each of this CTA's positions -> pushed to the row's home CTA
-        for (uint32_t p = tid; p < len; p += VT) {
-            const uint32_t row = Oj[p];
+        constexpr int PU = 4;  // order loads in flight per thread
+        for (uint32_t p0 = tid; p0 < len; p0 += VT * PU) {
+          uint32_t rows[PU];
+#pragma unroll
+          for (int u = 0; u < PU; ++u) {
+            const uint32_t p = p0 + u * VT;
+            rows[u] = p < len ? Oj[p] : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < PU; ++u) {
+            const uint32_t p = p0 + u * VT;
+            if (p >= len) continue;
+            const uint32_t row = rows[u];
             double T;
             if ((bits[p >> 5] >> (p & 31)) & 1u) {
                 T = A[p];
@@ -290,6 +301,7 @@ __global__ void __launch_bounds__(VT, 1) k_var_w(BlockState* st, const Seg* segs
             const uint32_t h = row / SL, slot = row - h * SL;
             if (col == 0) *cluster.map_shared_rank(wacc + slot, h) = wj;
             else dsmem_add_f64(wacc + slot, h, wj);
+          }
         }
         mark(3);
     }
@@ -317,33 +329,68 @@ __global__ void __launch_bounds__(VT, 1) k_var_w(BlockState* st, const Seg* segs
 // ------------------------------------------------------------ pass 2 (global)
 // Same steps through HBM for blocks larger than a cluster holds: pass 1 has
 // already placed cross_j in sorted order; suffix-scan it, then gather.
-__global__ void __launch_bounds__(1024) k_suffix_g(const BlockState* st, const Seg* segs, int nseg,
-                                                  const uint8_t* use, uint64_t n_rows, double* A) {
-    const int m = blockIdx.x % nseg;
-    const int col = blockIdx.x / nseg;
-    if (!use[m] || st[m].status != kConverged) return;
+// Tile-parallel segmented suffix scan (deterministic): tile sums, a
+// per-(block, column) suffix over its tiles, then each tile's own scan.
+__global__ void __launch_bounds__(FT) k_tsum_g(const BlockState* st, const Seg* segs, int nseg, const uint8_t* use,
+                                              uint64_t n_rows, const double* A, double* tsum, uint32_t ntiles) {
+    const uint32_t tile = blockIdx.x, col = blockIdx.y;
+    const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
-    double* a = A + static_cast<uint64_t>(col) * n_rows + S.begin;
-    const uint32_t n = S.n;
-    const uint32_t chunk = (n + blockDim.x - 1) / blockDim.x;
-    const uint32_t b0 = min(n, threadIdx.x * chunk), b1 = min(n, b0 + chunk);
-    double local = 0.0;
-    for (uint32_t q = b1; q-- > b0;) local += a[q];
-    __shared__ double s_tot[1024];
-    s_tot[threadIdx.x] = local;
-    __syncthreads();
-    for (int o = 1; o < static_cast<int>(blockDim.x); o <<= 1) {
-        double add = 0.0;
-        if (threadIdx.x + o < blockDim.x) add = s_tot[threadIdx.x + o];
-        __syncthreads();
-        s_tot[threadIdx.x] += add;
-        __syncthreads();
+    if (!use[m] || st[m].status != kConverged) return;
+    const uint32_t base = (tile - S.tile0) * FTILE, cnt = min(FTILE, S.n - base);
+    const double* a = A + static_cast<uint64_t>(col) * n_rows + S.begin + base;
+    double v[1] = {0.0};
+    for (uint32_t q = threadIdx.x; q < cnt; q += FT) v[0] += a[q];
+    __shared__ double sh[FT / 32];
+    block_sum<1>(v, sh);
+    if (threadIdx.x == 0) tsum[col * ntiles + tile] = v[0];
+}
+
+__global__ void k_tscan_g(const BlockState* st, const Seg* segs, int nseg, const uint8_t* use, const double* tsum,
+                          double* toff, uint32_t ntiles) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= 2 * nseg) return;
+    const int seg = m % nseg, col = m / nseg;
+    if (!use[seg] || st[seg].status != kConverged) return;
+    const Seg S = segs[seg];
+    const uint32_t nt = (S.n + FTILE - 1) / FTILE;
+    double run = 0.0;  // mass of the tiles above
+    for (uint32_t q = nt; q-- > 0;) {
+        toff[col * ntiles + S.tile0 + q] = run;
+        run += tsum[col * ntiles + S.tile0 + q];
     }
-    double run = threadIdx.x + 1 < blockDim.x ? s_tot[threadIdx.x + 1] : 0.0;
-    for (uint32_t q = b1; q-- > b0;) {
-        const double x = a[q];
-        run += x;
-        a[q] = with_flag(run, flag_of(x));  // the run-start flag stays with its position
+}
+
+__global__ void __launch_bounds__(FT) k_tapply_g(const BlockState* st, const Seg* segs, int nseg, const uint8_t* use,
+                                                uint64_t n_rows, double* A, const double* toff, uint32_t ntiles) {
+    const uint32_t tile = blockIdx.x, col = blockIdx.y;
+    const int m = seg_of_tile(segs, nseg, tile);
+    const Seg S = segs[m];
+    if (!use[m] || st[m].status != kConverged) return;
+    const uint32_t base = (tile - S.tile0) * FTILE, cnt = min(FTILE, S.n - base);
+    double* a = A + static_cast<uint64_t>(col) * n_rows + S.begin + base;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr uint32_t WL = FTILE / (FT / 32);  // contiguous elements per warp
+    const uint32_t w0 = min(cnt, wid * WL), w1 = min(cnt, w0 + WL);
+    double wsum = 0.0;
+    for (uint32_t q = w0 + lane; q < w1; q += 32) wsum += a[q];
+    wsum = warp_sum(wsum);
+    __shared__ double s_wt[FT / 32];
+    if (lane == 0) s_wt[wid] = wsum;
+    __syncthreads();
+    double carry = toff[col * ntiles + tile];
+    for (int w = wid + 1; w < FT / 32; ++w) carry += s_wt[w];
+    for (uint32_t t = (w1 - w0 + 31) / 32; t-- > 0;) {
+        const uint32_t q = w0 + t * 32 + lane;
+        const double x0 = q < w1 ? a[q] : 0.0;
+        double x = x0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_down_sync(0xffffffffu, x, o);
+            if (lane + o < 32) x += y;
+        }
+        if (q < w1) a[q] = with_flag(carry + x, flag_of(x0));  // the run-start flag stays with its position
+        carry += __shfl_sync(0xffffffffu, x, 0);
     }
 }
 
@@ -452,10 +499,14 @@ void launch_var_w(Ctx& c, const VarPlan& p, const VarIO& v, const int* seg_list,
 
 void launch_var_global(Ctx& c, const VarIO& v, const uint8_t* use, double* zb, double* Ag) {
     const int K = static_cast<int>(v.off->size() - 1);
-    k_suffix_g<<<2 * K, 1024, 0, c.stream>>>(v.st, v.segs, K, use, v.n_rows, Ag);
+    auto* tsum = c.ws.get_t<double>("var.tsum", 2 * static_cast<size_t>(v.tiles));
+    auto* toff = c.ws.get_t<double>("var.toff", 2 * static_cast<size_t>(v.tiles));
+    k_tsum_g<<<dim3(v.tiles, 2), FT, 0, c.stream>>>(v.st, v.segs, K, use, v.n_rows, Ag, tsum, v.tiles);
+    k_tscan_g<<<(2 * K + 127) / 128, 128, 0, c.stream>>>(v.st, v.segs, K, use, tsum, toff, v.tiles);
+    k_tapply_g<<<dim3(v.tiles, 2), FT, 0, c.stream>>>(v.st, v.segs, K, use, v.n_rows, Ag, toff, v.tiles);
     k_var_gather_g<<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, use, v.rp, v.n_rows, zb, Ag, v.partials,
                                                  v.tickets);
-    c.count_launch(2);
+    c.count_launch(4);
 }
 
 }  // namespace
