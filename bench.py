@@ -304,9 +304,11 @@ def run_ours(args):
         # prepare: read 2 packed ranks; write T (f64 pair) + its fp32 warm-up copy (Archimedean)
         add("k_prepare", st_.get("prepare", 0.0), 1, (16.0 if name == "gaussian" else 40.0) * rows, 0.0)
         vp = st_.get("var_point_ms", 0.0)
-        # variance pass 1: read ranks (+T for Gumbel); write score + two sorted cross values
-        add("k_var_point", vp, 1, (56.0 if name == "gumbel" else 40.0) * rows, F_VAR[name] * rows)
-        add("k_var_w", st_.get("variance", 0.0) - vp, 1, 32.0 * rows, 0.0)
+        # variance pass 1: read ranks + routes (+T for Gumbel); write score + two routed cross values
+        add("k_var_point", vp, 1, (64.0 if name == "gumbel" else 48.0) * rows, F_VAR[name] * rows)
+        # passes 2-3: scan reads cross + local position, writes W per slot (2 x 18 B);
+        # final reads route, score, W_1, W_2 (32 B)
+        add("k_var_scan+final", st_.get("variance", 0.0) - vp, 2, 68.0 * rows, 0.0)
         if "lik" in kernels[name]:
             lk = kernels[name]["lik"]
             add("k_lik(fp64)", lk["ms"], lk["launches"], B_PASS * rows * lk["fp64_passes"],

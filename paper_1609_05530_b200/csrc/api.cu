@@ -138,7 +138,6 @@ struct RankBufs {
 RankBufs rank_buffers(pcb::Ctx& c, uint64_t n_rows, uint64_t n_seg) {
     RankBufs b;
     b.r.rp = c.ws.get_t<unsigned long long>("pipe.rp", 2 * n_rows);
-    b.r.ord = c.ws.get_t<uint32_t>("pipe.ord", 2 * n_rows);
     b.bad = c.ws.get_t<int32_t>("pipe.bad", n_seg);
     PCB_CUDA(cudaMemsetAsync(b.bad, 0, n_seg * sizeof(int32_t), c.stream));
     return b;
@@ -170,7 +169,7 @@ void pipeline_blocks(pcb::Ctx& c, int fam, int prec, const double* d1, const dou
     io.n_rows = n_rows;
     io.off = off;
     io.rp = rb.r.rp;
-    io.ord = rb.r.ord;
+    io.rank = &rb.r;
     io.bad = rb.bad;
     pcb::run_fit(c, io, d_out);
     finish_stage_times(c);
@@ -375,7 +374,7 @@ int pcb_fit(pcb_context* ctx, int family, int precision, const double* u1, const
         io.u1 = d1;
         io.u2 = d2;
         io.rp = rb.r.rp;
-        io.ord = rb.r.ord;
+        io.rank = &rb.r;
         DevOut<pcb_fit_result> o(c, out, n_seg, "fit");
         pcb::run_fit(c, io, o.dev);
         finish_stage_times(c);
@@ -414,7 +413,7 @@ int pcb_asymptotic_variance(pcb_context* ctx, int family, const double* theta_ha
         io.u1 = d1;
         io.u2 = d2;
         io.rp = rb.r.rp;
-        io.ord = rb.r.ord;
+        io.rank = &rb.r;
         io.theta_in = dth;
         io.do_fit = false;
         auto* rec = c.ws.get_t<pcb_fit_result>("var.rec", n_seg);

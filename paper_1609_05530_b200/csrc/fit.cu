@@ -666,7 +666,7 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
         v.tiles = tiles;
         v.st = st;
         v.rp = io.rp;
-        v.ord = io.ord;
+        v.rank = io.rank;
         v.u1 = io.u1;
         v.u2 = io.u2;
         v.T64 = ((fam == kGaussian && !gtab) || (fam == kGumbel && !fp32T)) ? static_cast<const double2*>(T) : nullptr;

@@ -96,15 +96,27 @@ struct Ctx {
 //   bit  63    pos is the first position of its tie run
 // The run-start bits of a segment, set at the positions, mark where every
 // tie run begins; the variance finds a run's first position from them.
+// Cluster-ranked blocks also leave the route of their all-to-all (the
+// variance reuses it as a pre-planned, semi-coalesced permutation):
+//   route [2][n_rows] u32 : (owner CTA << 16) | receive slot of each element
+//   posl  [2][K][cl][rcap] u16 : owner-local sorted position (15 bits) |
+//                               run-start bit, per receive slot
+//   ocnt  [2][K][cl] u32 : elements each owner received
+//   routed[m] : both columns of block m went through the cluster path
 struct RankOut {
-    unsigned long long* rp;
-    uint32_t* ord;  // [2][n_rows]: sorted position -> row within the segment (the stable order)
+    unsigned long long* rp = nullptr;
+    uint32_t* route = nullptr;
+    uint16_t* posl = nullptr;
+    uint32_t* ocnt = nullptr;
+    int cl = 0;
+    uint32_t rcap = 0;
+    std::vector<uint8_t> routed;
 };
 
 // Ranks both columns of every segment. `bad` (n_seg int32, device) is set
 // non-zero for segments with non-finite values (validate_data).
 void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_rows, const std::vector<uint64_t>& off,
-               RankOut out, int32_t* d_bad);
+               RankOut& out, int32_t* d_bad);
 
 // u = (0.5*r2) * (1/(n_m+1)), bit-exact to normalized_rank_column
 void ranks_to_u(Ctx& c, const unsigned long long* rp, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
@@ -119,7 +131,7 @@ struct FitIO {
     // packed ranks [2][n_rows] (always: the variance needs the stable
     // positions); (u, v) come from u1/u2 when given, else from the ranks
     const unsigned long long* rp = nullptr;
-    const uint32_t* ord = nullptr;
+    const RankOut* rank = nullptr;  // route space of cluster-ranked blocks (may be null)
     const double* u1 = nullptr;
     const double* u2 = nullptr;
     const int32_t* bad = nullptr;  // per segment, may be null
@@ -142,7 +154,7 @@ struct VarIO {
     uint32_t tiles = 0;
     BlockState* st = nullptr;
     const unsigned long long* rp = nullptr;
-    const uint32_t* ord = nullptr;
+    const RankOut* rank = nullptr;
     const double* u1 = nullptr;
     const double* u2 = nullptr;
     const double2* T64 = nullptr;  // hoisted (x,y) (Gaussian) / (ln(-ln u), ln(-ln v)) (Gumbel fp64), or null

@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(RT) k_scatter(const RankRange* rr, int nr, con
 // by counting inside the bucket (L1-resident neighbours).
 __global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const unsigned long long* dkey,
                                             const uint32_t* didx, const uint32_t* hist, const uint32_t* bstart,
-                                            uint64_t n_rows, unsigned long long* o_rp, uint32_t* o_ord) {
+                                            uint64_t n_rows, unsigned long long* o_rp) {
     const int r = range_of_tile(rr, nr, blockIdx.x);
     const RankRange R = rr[r];
     const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
@@ -318,7 +318,6 @@ __global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const 
         }
         const uint64_t o = static_cast<uint64_t>(R.col) * n_rows + R.out_base + id;
         o_rp[o] = pack_rank(2u * lt + eq + 1u, pos, R.mode == 2 ? pos == R.run_start : pos == lt);
-        o_ord[static_cast<uint64_t>(R.col) * n_rows + R.out_base + pos] = id;
     }
 }
 
@@ -358,6 +357,7 @@ uint32_t tiles_of(uint64_t n) { return static_cast<uint32_t>((n + RTILE - 1) / R
 constexpr int CT = 1024;  // threads per cluster CTA
 constexpr int NWARP = CT / 32;
 constexpr int EMAX = 16;         // slice elements per thread (slice <= 16K)
+constexpr int QMAX = 16;         // received elements per thread (RCAP <= QMAX * CT)
 constexpr int kIdxBits = 18;     // row within the block (< 2^18) | local bucket in the high bits
 constexpr uint32_t kIdxMask = (1u << kIdxBits) - 1u;
 constexpr int kMaxCluster = 16;
@@ -401,7 +401,7 @@ inline ClusterPlan plan_cluster(uint64_t nmax) {
     for (int cl = 1; cl <= kMaxCluster; ++cl) {
         if (forced && cl != forced) continue;
         ClusterPlan p = plan_for(nmax, cl);
-        if (p.rcap < 65535 && p.smem <= kSmemLimit && p.s <= static_cast<uint32_t>(EMAX * CT) &&
+        if (p.rcap <= static_cast<uint32_t>(QMAX * CT) && p.rcap < 32768 && p.smem <= kSmemLimit && p.s <= static_cast<uint32_t>(EMAX * CT) &&
             nmax <= kIdxMask && (p.lg_nbl + kIdxBits) <= 32 && (static_cast<uint64_t>(cl) << p.lg_nbl) <= 65536)
             return p;
     }
@@ -454,9 +454,10 @@ __device__ void block_scan_excl_u16(uint32_t* cw, uint16_t* start, uint32_t n, u
 }
 
 __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, const double* c0, const double* c1,
-                                                       uint64_t n_rows, unsigned long long* rp, uint32_t* ord,
-                                                       int32_t* fb, int32_t* bad, int CL, uint32_t RCAP,
-                                                       uint32_t lg_nbl, unsigned long long* prof) {
+                                                       uint64_t n_rows, unsigned long long* rp, uint32_t* route,
+                                                       uint16_t* posl_g, uint32_t* ocnt, uint32_t K, int32_t* fb,
+                                                       int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
+                                                       unsigned long long* prof) {
     namespace cg = cooperative_groups;
     long long t_prev = clock64();
     auto mark = [&](int k) {  // optional phase timing (PCB_RANK_PROFILE): thread 0's clock deltas
@@ -562,12 +563,14 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     const bool constant = s_gmin == s_gmax;
     if (constant || !(isfinite(scale) && scale > 0.0 && isfinite(hm))) {
         if (constant && !isfinite(vmin)) {
-            if (r == 0 && tid == 0) bad[J.seg] = 1;
-        } else if (constant) {  // one tie run: avg rank (n+1)/2 for all, stable positions = row order
-            for (uint32_t i = a + tid; i < e; i += CT) {
-                rp[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = pack_rank(J.n + 1u, i, i == 0);
-                ord[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = i;
+            if (r == 0 && tid == 0) {
+                bad[J.seg] = 1;
+                fb[jid] = 2;  // handled, no route
             }
+        } else if (constant) {  // one tie run: avg rank (n+1)/2 for all, stable positions = row order
+            for (uint32_t i = a + tid; i < e; i += CT)
+                rp[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = pack_rank(J.n + 1u, i, i == 0);
+            if (r == 0 && tid == 0) fb[jid] = 2;  // ranked, no route
         } else if (r == 0 && tid == 0) {
             fb[jid] = 1;
         }
@@ -612,7 +615,10 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     }
     __syncthreads();
     if (s_gbad) {
-        if (r == 0 && tid == 0) bad[J.seg] = 1;
+        if (r == 0 && tid == 0) {
+            bad[J.seg] = 1;
+            fb[jid] = 2;
+        }
         cluster.sync();
         return;
     }
@@ -654,6 +660,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
             const uint32_t b = (bk[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
             const uint32_t d = b >> lg_nbl;
             const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
+            route[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = (d << 16) | slot;  // owner, receive slot
             *cluster.map_shared_rank(recv_key + slot, d) = kk;
             *cluster.map_shared_rank(recv_idx + slot, d) = ((b & lmask) << kIdxBits) | i;
         }
@@ -681,13 +688,19 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     mark(4);
     // ---- 5. rank inside each bucket; write packed (r2 | pos | run-start)
     unsigned long long* out = rp + static_cast<uint64_t>(J.col) * n_rows + J.begin;
-    uint32_t* ordo = ord + static_cast<uint64_t>(J.col) * n_rows + J.begin;
+    // this owner's region of the route space: local sorted position (15 bits) | run-start bit
+    uint16_t* po = posl_g + ((static_cast<uint64_t>(J.col) * K + J.seg) * CL + r) * RCAP;
+    if (tid == 0) ocnt[(static_cast<uint64_t>(J.col) * K + J.seg) * CL + r] = T;
     // walk the elements in bucket order: a warp's lanes mostly share buckets, so
-    // the bucket-mate loads are shared-memory broadcasts and the order writes
-    // are nearly contiguous
-    for (uint32_t qq = tid; qq < T; qq += CT) {
+    // the bucket-mate loads are shared-memory broadcasts. (slot, local position)
+    // pairs stay in registers until perm is free, then go out in slot order.
+    uint32_t keep[QMAX];
+#pragma unroll
+    for (int k = 0; k < QMAX; ++k) {
+        const uint32_t qq = tid + k * CT;
+        if (qq >= T) break;
         const uint32_t j = perm[qq];
-        const unsigned long long k = recv_key[j];
+        const unsigned long long kv = recv_key[j];
         const uint32_t id = recv_idx[j];  // (local bucket << kIdxBits) | row: same bucket => compares as row
         const uint32_t lb = id >> kIdxBits;
         const uint32_t s0 = lhs[lb], s1 = lhs[lb + 1];
@@ -696,21 +709,28 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
         for (uint32_t q = s0; q < s1; ++q) {
             const uint32_t o = perm[q];
             const unsigned long long kq = recv_key[o];
-            less += kq < k;
-            const bool eqk = kq == k;
+            less += kq < kv;
+            const bool eqk = kq == kv;
             same += eqk;
             before += eqk && recv_idx[o] < id;
         }
         const uint32_t lt = base + s0 + less;
         out[id & kIdxMask] = pack_rank(2u * lt + same + 1u, lt + before, before == 0);
-        ordo[lt + before] = id & kIdxMask;
+        keep[k] = (j << 16) | (lt + before - base) | (before == 0 ? 0x8000u : 0u);
     }
+    __syncthreads();  // perm is free
+#pragma unroll
+    for (int k = 0; k < QMAX; ++k) {
+        if (tid + k * CT >= T) break;
+        perm[keep[k] >> 16] = static_cast<uint16_t>(keep[k] & 0xffffu);
+    }
+    __syncthreads();
+    for (uint32_t j = tid; j < T; j += CT) po[j] = perm[j];
     mark(5);
 }
 
 void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, uint32_t njobs, const double* c0,
-                         const double* c1, uint64_t n_rows, unsigned long long* rp, uint32_t* ord, int32_t* fb,
-                         int32_t* bad) {
+                         const double* c1, uint64_t n_rows, RankOut& out, int32_t* fb, int32_t* bad) {
     PCB_CUDA(cudaFuncSetAttribute(k_rank_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(p.smem)));
     if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(k_rank_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -731,8 +751,8 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
         prof = c.ws.get_t<unsigned long long>("rank.prof", 8);
         PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
     }
-    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, rp, ord, fb, bad, p.cl, p.rcap, p.lg_nbl,
-                                prof));
+    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, out.rp, out.route, out.posl, out.ocnt,
+                                njobs / 2, fb, bad, p.cl, p.rcap, p.lg_nbl, prof));
     if (prof) {
         unsigned long long h[8];
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
@@ -813,7 +833,7 @@ void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64
         k_scan<<<nr, 1024, 0, st>>>(d_rr, hist, bstart, cursor, ov, ovn, ov_cap);
         if (l0) k_scatter<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
         else k_scatter<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
-        k_rank<<<ntiles, RT, 0, st>>>(d_rr, nr, dkey, didx, hist, bstart, n_rows, out.rp, out.ord);
+        k_rank<<<ntiles, RT, 0, st>>>(d_rr, nr, dkey, didx, hist, bstart, n_rows, out.rp);
         c.count_launch(6);
         PCB_CUDA(cudaMemcpyAsync(h_ovn, ovn, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         PCB_CUDA(cudaStreamSynchronize(st));
@@ -879,7 +899,7 @@ void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64
 }  // namespace
 
 void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_rows, const std::vector<uint64_t>& off,
-               RankOut out, int32_t* d_bad) {
+               RankOut& out, int32_t* d_bad) {
     const size_t K = off.size() - 1;
     if (K == 0 || n_rows == 0) return;
     uint64_t nmax = 0;
@@ -902,13 +922,23 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
         }
         PCB_CUDA(cudaMemcpyAsync(jobs, hj.data(), njobs * sizeof(ClusterJob), cudaMemcpyHostToDevice, c.stream));
         PCB_CUDA(cudaMemsetAsync(fb, 0, njobs * sizeof(int32_t), c.stream));
-        launch_rank_cluster(c, plan, jobs, njobs, d_col1, d_col2, n_rows, out.rp, out.ord, fb, d_bad);
+        out.cl = plan.cl;
+        out.rcap = plan.rcap;
+        out.route = c.ws.get_t<uint32_t>("rank.route", 2 * n_rows);
+        out.posl = c.ws.get_t<uint16_t>("rank.posl", static_cast<size_t>(njobs) * plan.cl * plan.rcap);
+        out.ocnt = c.ws.get_t<uint32_t>("rank.ocnt", static_cast<size_t>(njobs) * plan.cl);
+        launch_rank_cluster(c, plan, jobs, njobs, d_col1, d_col2, n_rows, out, fb, d_bad);
         std::vector<int32_t> hfb(njobs);
         PCB_CUDA(cudaMemcpyAsync(hfb.data(), fb, njobs * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
         PCB_CUDA(cudaStreamSynchronize(c.stream));
-        for (uint32_t j = 0; j < njobs; ++j)
-            if (hfb[j]) fallback.push_back(j);
+        out.routed.assign(K, 1);
+        for (uint32_t j = 0; j < njobs; ++j) {
+            if (hfb[j]) out.routed[j % K] = 0;
+            if (hfb[j] == 1) fallback.push_back(j);
+        }
     } else {
+        out.cl = 0;
+        out.routed.assign(K, 0);
         for (uint32_t j = 0; j < 2 * K; ++j) fallback.push_back(j);
     }
     run_ranks_global(c, d_col1, d_col2, n_rows, off, fallback, out, d_bad);

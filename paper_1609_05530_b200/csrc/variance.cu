@@ -11,13 +11,18 @@
 //
 // Pass 1 (k_var_point, grid of tiles, FP64-bound): per-point log c, score,
 //   Hessian, cross_1, cross_2 at theta-hat in point order (coalesced), and the
-//   block sums I, C_1, C_2, loglik.
-// Pass 2 (k_var_w, one thread-block cluster per block): column by column,
-//   cross_j is scattered to its sorted position in the cluster's distributed
-//   shared memory together with a run-start bitmap, suffix-scanned in place,
-//   and gathered back at each point's run start; M-hat and sigma2 follow.
-//   HBM sees only the per-point arrays; the permutation traffic is DSMEM.
-// Blocks too large for one cluster take the same steps through global memory.
+//   block sums I, C_1, C_2, loglik. cross_j leaves along the route the rank
+//   stage's all-to-all took (owner CTA, receive slot): a warp's 32 consecutive
+//   rows land in a few short runs of slots, so the scatter is semi-coalesced.
+// Pass 2 (k_var_scan, one thread-block cluster per block, the rank stage's
+//   owners): each owner loads its received slots (coalesced), places them at
+//   their owner-local sorted positions in shared memory, suffix-scans with the
+//   higher owners' totals as carry (the only DSMEM traffic: CL doubles), and
+//   writes W_j back per slot (coalesced). Tie runs never straddle owners.
+// Pass 3 (k_var_final, grid of tiles): z = score + W_1 + W_2 per row through
+//   the route, sum z^2 -> M-hat -> sigma2.
+// Blocks the rank stage did not route (global-path ranks, constant columns)
+// take the same steps through sorted-order arrays in global memory.
 // Deterministic: positions are unique, scans and sums run in fixed order.
 #include <cooperative_groups.h>
 
@@ -37,8 +42,6 @@ namespace cg = cooperative_groups;
 
 constexpr int VT = 1024;  // threads per cluster CTA
 constexpr int VNW = VT / 32;
-constexpr int kMaxCl = 16;
-constexpr size_t kVarSmem = 227 * 1024 - 4096;  // static shared memory lives beside it
 
 // Per-theta constants, built once per CTA (they cost more than a point).
 template <int FAM>
@@ -85,8 +88,9 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
                                                  const double* __restrict__ u1, const double* __restrict__ u2,
                                                  const double2* __restrict__ T64, const double* __restrict__ gtab,
                                                  const uint64_t* goff, uint64_t n_rows, double* __restrict__ zb,
-                                                 double* __restrict__ Ag, double* partials,
-                                                 unsigned* tickets) {
+                                                 double* __restrict__ Ag, const uint8_t* __restrict__ routed,
+                                                 const uint32_t* __restrict__ route, double* __restrict__ xr,
+                                                 uint32_t CL, uint32_t RCAP, double* partials, unsigned* tickets) {
     const uint32_t tile = blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
@@ -96,10 +100,14 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
     const uint32_t base = (tile - S.tile0) * FTILE;
     const double* gt = gtab ? gtab + goff[m] : nullptr;
     const bool has_t = gt || T64;
+    const bool rt = routed && routed[m];
+    double* x1 = rt ? xr + static_cast<uint64_t>(m) * CL * RCAP : nullptr;
+    double* x2 = rt ? xr + (static_cast<uint64_t>(nseg) + m) * CL * RCAP : nullptr;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     constexpr int U = 2;  // points per thread in flight
     for (int k0 = 0; k0 < PPT; k0 += U) {
         unsigned long long p1[U], p2[U];
+        uint32_t r1[U], r2[U];
         double2 tt[U];
         double uu[U], ww[U];
 #pragma unroll
@@ -114,6 +122,10 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
                     ww[j] = u2[row];
                 }
                 if (T64) tt[j] = T64[row];
+                if (rt) {
+                    r1[j] = route[row];
+                    r2[j] = route[n_rows + row];
+                }
             }
         }
 #pragma unroll
@@ -128,11 +140,14 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
             if (gt) tt[j] = make_double2(gt[rank_r2(p1[j])], gt[rank_r2(p2[j])]);
             const PointFull p = eval_point<FAM>(th, u, w, tt[j], has_t);
             zb[row] = p.score;
-            // cross_j to its sorted position (random within the block: L2-resident
-            // while the block's tiles are in flight), run-start flag beside it
-            const uint64_t q1 = S.begin + rank_pos(p1[j]), q2 = n_rows + S.begin + rank_pos(p2[j]);
-            Ag[q1] = with_flag(p.cross1, rank_first(p1[j]));
-            Ag[q2] = with_flag(p.cross2, rank_first(p2[j]));
+            if (rt) {  // cross_j to (owner, slot) of the rank stage's route
+                x1[(r1[j] >> 16) * RCAP + (r1[j] & 0xffffu)] = p.cross1;
+                x2[(r2[j] >> 16) * RCAP + (r2[j] & 0xffffu)] = p.cross2;
+            } else {  // cross_j to its sorted position, run-start flag beside it
+                const uint64_t q1 = S.begin + rank_pos(p1[j]), q2 = n_rows + S.begin + rank_pos(p2[j]);
+                Ag[q1] = with_flag(p.cross1, rank_first(p1[j]));
+                Ag[q2] = with_flag(p.cross2, rank_first(p2[j]));
+            }
             v[0] += p.hess;
             v[1] += u * p.cross1;
             v[2] += w * p.cross2;
@@ -158,22 +173,13 @@ __device__ __forceinline__ double finish_sigma2(BlockState& s, double zz, double
     return (zz / nd) / (info * info) / nd;
 }
 
-// ------------------------------------------------------------ pass 2 (cluster)
-// W_j(row) += value on the row's home CTA (DSMEM reduction; each row gets
-// one store for column 1 and one add for column 2, so the result is exact
-// and order-independent).
-__device__ __forceinline__ void dsmem_add_f64(double* local_slot, uint32_t rank, double v) {
-    const uint32_t la = static_cast<uint32_t>(__cvta_generic_to_shared(local_slot));
-    uint32_t ra;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
-    asm volatile("red.relaxed.cluster.shared::cluster.add.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
-}
-
-template <int DUMMY>
-__global__ void __launch_bounds__(VT, 1) k_var_w(BlockState* st, const Seg* segs, const int* seg_list,
-                                                const uint32_t* __restrict__ ord, uint64_t n_rows,
-                                                const double* __restrict__ zb, const double* __restrict__ Ag, int CL,
-                                                uint32_t SMAX, unsigned long long* prof) {
+// ------------------------------------------------------------ pass 2 (routed)
+// Cluster of the block's CL owners; CTA r holds owner r's slots. Per column:
+// place, suffix-scan with carry from owners above, W per slot in place.
+__global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const int* seg_list, int nseg,
+                                                   const Seg* segs, const uint16_t* __restrict__ posl,
+                                                   const uint32_t* __restrict__ ocnt, double* __restrict__ xr, int CL,
+                                                   uint32_t RCAP, unsigned long long* prof) {
     long long t_prev = clock64();
     auto mark = [&](int k) {  // optional phase timing (PCB_VAR_PROFILE)
         if (prof && threadIdx.x == 0) {
@@ -185,58 +191,58 @@ __global__ void __launch_bounds__(VT, 1) k_var_w(BlockState* st, const Seg* segs
     cg::cluster_group cluster = cg::this_cluster();
     const int r = static_cast<int>(cluster.block_rank());
     const int m = seg_list[blockIdx.x / CL];
-    const Seg S = segs[m];
     if (st[m].status != kConverged) return;  // uniform across the cluster, before any DSMEM access
-    const uint32_t n = S.n;
-    const uint32_t SL = (n + CL - 1) / CL;
-    const uint32_t a = min(n, r * SL), e = min(n, a + SL);
-    const uint32_t len = e - a;
+    const double nd = static_cast<double>(segs[m].n);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const double nd = static_cast<double>(n);
 
-    // CTA r owns sorted positions [a, e) AND home rows [a, e) of the block
     extern __shared__ __align__(16) unsigned char smem[];
-    double* A = reinterpret_cast<double*>(smem);               // suffix sums of its positions
-    double* wacc = A + SMAX;                                   // W_1 + W_2 of its home rows
-    uint32_t* bits = reinterpret_cast<uint32_t*>(wacc + SMAX);  // run-start bit per position
-    __shared__ double s_tot, s_z;
-    __shared__ double s_red[VNW];
+    double* A = reinterpret_cast<double*>(smem);                 // owner-local sorted positions
+    uint32_t* bits = reinterpret_cast<uint32_t*>(A + RCAP);      // run-start bit per position
+    __shared__ double s_tot;
     __shared__ double s_wt[VNW], s_wo[VNW];
-
-    // warp w owns the contiguous positions [w*WL, (w+1)*WL) of the slice (WL % 32 == 0)
-    const uint32_t WL = ((len + VNW - 1) / VNW + 31) & ~31u;
-    const uint32_t w0 = min(len, wid * WL), w1 = min(len, w0 + WL);
 
     for (int col = 0; col < 2; ++col) {
         const double cj = col ? st[m].c2 : st[m].c1;
-        const double* Aj = Ag + static_cast<uint64_t>(col) * n_rows + S.begin + a;
-        const uint32_t* Oj = ord + static_cast<uint64_t>(col) * n_rows + S.begin + a;
-        cluster.sync();  // the previous column's walks over A / bits are done everywhere
+        const uint64_t reg = ((static_cast<uint64_t>(col) * nseg + m) * CL + r) * RCAP;
+        const uint32_t T = ocnt[(static_cast<uint64_t>(col) * nseg + m) * CL + r];
+        double* X = xr + reg;
+        const uint16_t* P = posl + reg;
+        cluster.sync();  // the previous column is finished everywhere (s_tot, A, bits reusable)
         mark(0);
-        // load this warp's positions (coalesced), peel the run-start bits, warp total
-        double wsum = 0.0;
-        for (uint32_t q0 = w0; q0 < w1; q0 += 32 * 4) {
-            double c[4];
+        for (uint32_t q = tid; q <= T / 32; q += VT) bits[q] = 0u;
+        __syncthreads();
+        // place: coalesced slot loads, random shared-memory stores
+        for (uint32_t j0 = tid; j0 < T; j0 += VT * 4) {
+            double x[4];
+            uint32_t pv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint32_t q = q0 + u * 32 + lane;
-                c[u] = q < w1 ? Aj[q] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t q = q0 + u * 32 + lane;
-                const unsigned fb = __ballot_sync(0xffffffffu, q < w1 && flag_of(c[u]));
-                if (q0 + u * 32 < w1) {
-                    if (lane == 0) bits[(q0 + u * 32) >> 5] = fb;
-                    if (q < w1) A[q] = c[u];
-                    wsum += c[u];
+                const uint32_t j = j0 + u * VT;
+                if (j < T) {
+                    x[u] = X[j];
+                    pv[u] = P[j];
                 }
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = j0 + u * VT;
+                if (j >= T) continue;
+                const uint32_t p = pv[u] & 0x7fffu;
+                A[p] = x[u];
+                if (pv[u] & 0x8000u) atomicOr(bits + (p >> 5), 1u << (p & 31));
+            }
         }
+        __syncthreads();
+        mark(1);
+        // warp w scans the contiguous positions [w*WL, (w+1)*WL)
+        const uint32_t WL = ((T + VNW - 1) / VNW + 31) & ~31u;
+        const uint32_t w0 = min(T, wid * WL), w1 = min(T, w0 + WL);
+        double wsum = 0.0;
+        for (uint32_t q = w0 + lane; q < w1; q += 32) wsum += A[q];
         wsum = warp_sum(wsum);
         if (lane == 0) s_wt[wid] = wsum;
         __syncthreads();
-        if (wid == 0) {  // exclusive suffix of the warp totals; slice total
+        if (wid == 0) {  // exclusive suffix of the warp totals; owner total
             double x = s_wt[lane];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -246,11 +252,9 @@ __global__ void __launch_bounds__(VT, 1) k_var_w(BlockState* st, const Seg* segs
             s_wo[lane] = x - s_wt[lane];
             if (lane == 0) s_tot = x;
         }
-        mark(1);
-        cluster.sync();  // slice totals published
+        cluster.sync();  // owner totals published
         double carry = s_wo[wid];
-        for (int q = r + 1; q < CL; ++q) carry += *cluster.map_shared_rank(&s_tot, q);  // slices above
-        // suffix scan of the warp's positions, top tile first
+        for (int q = r + 1; q < CL; ++q) carry += *cluster.map_shared_rank(&s_tot, q);  // owners above
         for (uint32_t t = (w1 - w0 + 31) / 32; t-- > 0;) {
             const uint32_t q = w0 + t * 32 + lane;
             double x = q < w1 ? A[q] : 0.0;
@@ -262,68 +266,85 @@ __global__ void __launch_bounds__(VT, 1) k_var_w(BlockState* st, const Seg* segs
             if (q < w1) A[q] = carry + x;
             carry += __shfl_sync(0xffffffffu, x, 0);
         }
-        cluster.sync();  // suffix sums complete everywhere
+        __syncthreads();
         mark(2);
-        // W_j of the row at each of this CTA's positions -> pushed to the row's home CTA
-        constexpr int PU = 4;  // order loads in flight per thread
-        for (uint32_t p0 = tid; p0 < len; p0 += VT * PU) {
-          uint32_t rows[PU];
-#pragma unroll
-          for (int u = 0; u < PU; ++u) {
-            const uint32_t p = p0 + u * VT;
-            rows[u] = p < len ? Oj[p] : 0u;
-          }
-#pragma unroll
-          for (int u = 0; u < PU; ++u) {
-            const uint32_t p = p0 + u * VT;
-            if (p >= len) continue;
-            const uint32_t row = rows[u];
-            double T;
-            if ((bits[p >> 5] >> (p & 31)) & 1u) {
-                T = A[p];
-            } else {  // tied, not first: highest run-start bit below this position
-                uint32_t t = a + p - 1;
-                uint32_t q;
+        // W_j per slot: suffix sum at the start of the slot's tie run (owner-local)
+        for (uint32_t j = tid; j < T; j += VT) {
+            const uint32_t pv = P[j];
+            uint32_t q = pv & 0x7fffu;
+            if (!(pv & 0x8000u)) {
+                uint32_t t = q - 1;  // position 0 of an owner always starts a run
                 for (;;) {
-                    const uint32_t o = t / SL, lt = t - o * SL;
-                    uint32_t w = *cluster.map_shared_rank(bits + (lt >> 5), o);
-                    w &= 0xffffffffu >> (31 - (lt & 31));
+                    const uint32_t w = bits[t >> 5] & (0xffffffffu >> (31 - (t & 31)));
                     if (w) {
-                        q = o * SL + (lt & ~31u) + (31 - __clz(w));
+                        q = (t & ~31u) + (31 - __clz(w));
                         break;
                     }
-                    t = o * SL + (lt & ~31u) - 1;  // position 0 always starts a run
+                    t = (t & ~31u) - 1;
                 }
-                const uint32_t o = q / SL;
-                T = *cluster.map_shared_rank(A + (q - o * SL), o);
             }
-            const double wj = (T - cj) / nd;
-            const uint32_t h = row / SL, slot = row - h * SL;
-            if (col == 0) *cluster.map_shared_rank(wacc + slot, h) = wj;
-            else dsmem_add_f64(wacc + slot, h, wj);
-          }
+            X[j] = (A[q] - cj) / nd;
         }
         mark(3);
     }
-    cluster.sync();  // every W has reached its home row
-    double zz = 0.0;
-    for (uint32_t i = tid; i < len; i += VT) {
-        const double z = zb[S.begin + a + i] + wacc[i];
-        zz += z * z;
+    cluster.sync();  // peers' s_tot reads are done
+}
+
+// z = score + W_1 + W_2 per row (through the route), sum z^2 -> sigma2
+__global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* segs, int nseg,
+                                                 const uint8_t* __restrict__ routed,
+                                                 const uint32_t* __restrict__ route, uint64_t n_rows,
+                                                 const double* __restrict__ zb, const double* __restrict__ xr,
+                                                 uint32_t CL, uint32_t RCAP, double* partials, unsigned* tickets) {
+    const uint32_t tile = blockIdx.x;
+    const int m = seg_of_tile(segs, nseg, tile);
+    const Seg S = segs[m];
+    if (!routed[m] || st[m].status != kConverged) return;
+    const double* x1 = xr + static_cast<uint64_t>(m) * CL * RCAP;
+    const double* x2 = xr + (static_cast<uint64_t>(nseg) + m) * CL * RCAP;
+    const uint32_t base = (tile - S.tile0) * FTILE;
+    double v[1] = {0.0};
+    constexpr int U = 4;
+    for (int k0 = 0; k0 < PPT; k0 += U) {
+        uint32_t r1[U], r2[U];
+        double zz[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            if (i < S.n) {
+                const uint64_t row = S.begin + i;
+                r1[j] = route[row];
+                r2[j] = route[n_rows + row];
+                zz[j] = zb[row];
+            }
+        }
+        double w1[U], w2[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            if (i < S.n) {
+                w1[j] = x1[(r1[j] >> 16) * RCAP + (r1[j] & 0xffffu)];
+                w2[j] = x2[(r2[j] >> 16) * RCAP + (r2[j] & 0xffffu)];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            if (i < S.n) {
+                double z = zz[j];
+                z += w1[j];
+                z += w2[j];
+                v[0] += z * z;
+            }
+        }
     }
-    // fixed-order reduction of sum z^2: block, then cluster
-    double v[1] = {zz};
-    block_sum<1>(v, s_red);
-    if (tid == 0) s_z = v[0];
-    cluster.sync();
-    if (r == 0 && tid == 0) {
-        double tot = 0.0;
-        for (int q = 0; q < CL; ++q) tot += *cluster.map_shared_rank(&s_z, q);
+    __shared__ double sh[FT / 32];
+    if (!tile_reduce<1>(v, sh, partials, tickets, S, m, tile)) return;
+    if (threadIdx.x == 0) {
         BlockState s = st[m];
-        s.sigma2 = finish_sigma2(s, tot, nd);
+        s.sigma2 = finish_sigma2(s, v[0], static_cast<double>(S.n));
         st[m] = s;
     }
-    cluster.sync();  // peers' shared memory is read above
 }
 
 // ------------------------------------------------------------ pass 2 (global)
@@ -431,50 +452,30 @@ __global__ void __launch_bounds__(FT) k_var_gather_g(BlockState* st, const Seg* 
     }
 }
 
-struct VarPlan {
-    int cl = 0;
-    uint32_t smax = 0;
-    size_t smem = 0;
-};
-
-VarPlan plan_var(uint64_t nmax) {
-    int forced = 0;
-    if (const char* v = std::getenv("PCB_VAR_CL")) forced = std::atoi(v);
-    if (const char* v = std::getenv("PCB_VAR_GLOBAL"))
-        if (v[0] && v[0] != '0') return VarPlan{};
-    for (int cl = 1; cl <= kMaxCl; ++cl) {
-        if (forced && cl != forced) continue;
-        VarPlan p;
-        p.cl = cl;
-        p.smax = static_cast<uint32_t>((nmax + cl - 1) / cl);
-        p.smax = (p.smax + 31u) & ~31u;
-        p.smem = static_cast<size_t>(p.smax) * 16 + (p.smax / 32 + 1) * 4;
-        if (p.smem <= kVarSmem) return p;
-    }
-    return VarPlan{};
-}
-
 template <int FAM>
-void launch_var_point(Ctx& c, const VarIO& v, double* zb, double* Ag) {
+void launch_var_point(Ctx& c, const VarIO& v, double* zb, double* Ag, const uint8_t* d_routed, double* xr) {
     const int K = static_cast<int>(v.off->size() - 1);
+    const RankOut* R = v.rank;
     k_var_point<FAM><<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, v.rp, v.u1, v.u2, v.T64, v.gtab, v.goff,
-                                                   v.n_rows, zb, Ag, v.partials, v.tickets);
+                                                   v.n_rows, zb, Ag, d_routed, R ? R->route : nullptr, xr,
+                                                   R ? R->cl : 0, R ? R->rcap : 0, v.partials, v.tickets);
     c.count_launch();
 }
 
-void launch_var_w(Ctx& c, const VarPlan& p, const VarIO& v, const int* seg_list, int njobs, double* zb,
-                  const double* Ag) {
-    auto k = k_var_w<0>;
-    PCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)));
-    if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+void launch_var_scan(Ctx& c, const VarIO& v, const int* seg_list, int njobs, double* xr) {
+    const RankOut& R = *v.rank;
+    const int K = static_cast<int>(v.off->size() - 1);
+    const size_t smem = static_cast<size_t>(R.rcap) * 8 + (R.rcap / 32 + 1) * 4;
+    PCB_CUDA(cudaFuncSetAttribute(k_var_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (R.cl > 8) PCB_CUDA(cudaFuncSetAttribute(k_var_scan, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(njobs) * static_cast<unsigned>(p.cl));
+    cfg.gridDim = dim3(static_cast<unsigned>(njobs) * static_cast<unsigned>(R.cl));
     cfg.blockDim = dim3(VT);
-    cfg.dynamicSmemBytes = p.smem;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = static_cast<unsigned>(p.cl);
+    attr[0].val.clusterDim.x = static_cast<unsigned>(R.cl);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -485,15 +486,17 @@ void launch_var_w(Ctx& c, const VarPlan& p, const VarIO& v, const int* seg_list,
         prof = c.ws.get_t<unsigned long long>("var.prof", 8);
         PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
     }
-    PCB_CUDA(cudaLaunchKernelEx(&cfg, k, v.st, v.segs, seg_list, v.ord, v.n_rows, zb, Ag, p.cl, p.smax, prof));
+    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_var_scan, static_cast<const BlockState*>(v.st), seg_list, K,
+                                static_cast<const Seg*>(v.segs), static_cast<const uint16_t*>(R.posl),
+                                static_cast<const uint32_t*>(R.ocnt), xr, R.cl, R.rcap, prof));
     c.count_launch();
     if (prof) {
         unsigned long long h[8];
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
         PCB_CUDA(cudaStreamSynchronize(c.stream));
-        const double ctas = static_cast<double>(njobs) * p.cl;
-        std::fprintf(stderr, "[var profile] CL=%d smax=%u cycles/CTA (both columns): sync %.0f  load %.0f  scan %.0f  gather %.0f\n",
-                     p.cl, p.smax, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas);
+        const double ctas = static_cast<double>(njobs) * R.cl;
+        std::fprintf(stderr, "[var profile] CL=%d rcap=%u cycles/CTA (both columns): sync %.0f  place %.0f  scan %.0f  W %.0f\n",
+                     R.cl, R.rcap, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas);
     }
 }
 
@@ -515,31 +518,47 @@ void run_variance(Ctx& c, const VarIO& v) {
     const std::vector<uint64_t>& off = *v.off;
     const int K = static_cast<int>(off.size() - 1);
     auto* zb = c.ws.get_t<double>("var.z", v.n_rows);
-    auto* Ag = c.ws.get_t<double>("var.A", 2 * v.n_rows);
-    PCB_CUDA(cudaEventRecord(c.ev[6], c.stream));
-    if (v.family == kGaussian) launch_var_point<kGaussian>(c, v, zb, Ag);
-    else if (v.family == kFrank) launch_var_point<kFrank>(c, v, zb, Ag);
-    else launch_var_point<kGumbel>(c, v, zb, Ag);
-    PCB_CUDA(cudaEventRecord(c.ev[7], c.stream));
-    uint64_t nmax = 0;
-    for (int m = 0; m < K; ++m) nmax = std::max<uint64_t>(nmax, off[m + 1] - off[m]);
-    const VarPlan p = plan_var(nmax);
-    if (p.cl > 0) {
-        std::vector<int> jobs(K);
-        for (int m = 0; m < K; ++m) jobs[m] = m;
-        int* d_jobs = c.ws.get_t<int>("var.jobs", K);
-        PCB_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), K * sizeof(int), cudaMemcpyHostToDevice, c.stream));
-        launch_var_w(c, p, v, d_jobs, K, zb, Ag);
-    } else {
-        std::vector<uint8_t> use(K, 1);
-        uint8_t* d_use = c.ws.get_t<uint8_t>("var.use", K);
-        PCB_CUDA(cudaMemcpyAsync(d_use, use.data(), K, cudaMemcpyHostToDevice, c.stream));
-        launch_var_global(c, v, d_use, zb, Ag);
+    // which blocks take the routed path (the rank stage's cluster route)
+    std::vector<uint8_t> routed(K, 0);
+    const char* vg = std::getenv("PCB_VAR_GLOBAL");
+    const bool force_global = vg && vg[0] && vg[0] != '0';
+    int nrouted = 0;
+    if (v.rank && v.rank->cl > 0 && !force_global && static_cast<int>(v.rank->routed.size()) == K)
+        for (int m = 0; m < K; ++m) nrouted += (routed[m] = v.rank->routed[m]);
+    const bool any_global = nrouted < K;
+    double* Ag = any_global ? c.ws.get_t<double>("var.A", 2 * v.n_rows) : nullptr;
+    double* xr = nrouted ? c.ws.get_t<double>("var.xr", 2 * static_cast<size_t>(K) * v.rank->cl * v.rank->rcap)
+                         : nullptr;
+    uint8_t* d_flags = c.ws.get_t<uint8_t>("var.flags", 2 * static_cast<size_t>(K));  // [routed | global]
+    std::vector<uint8_t> hflags(2 * K);
+    for (int m = 0; m < K; ++m) {
+        hflags[m] = routed[m];
+        hflags[K + m] = !routed[m];
     }
+    PCB_CUDA(cudaMemcpyAsync(d_flags, hflags.data(), 2 * K, cudaMemcpyHostToDevice, c.stream));
+    const uint8_t* d_routed = nrouted ? d_flags : nullptr;
+    PCB_CUDA(cudaEventRecord(c.ev[6], c.stream));
+    if (v.family == kGaussian) launch_var_point<kGaussian>(c, v, zb, Ag, d_routed, xr);
+    else if (v.family == kFrank) launch_var_point<kFrank>(c, v, zb, Ag, d_routed, xr);
+    else launch_var_point<kGumbel>(c, v, zb, Ag, d_routed, xr);
+    PCB_CUDA(cudaEventRecord(c.ev[7], c.stream));
+    if (nrouted) {
+        std::vector<int> jobs;
+        for (int m = 0; m < K; ++m)
+            if (routed[m]) jobs.push_back(m);
+        int* d_jobs = c.ws.get_t<int>("var.jobs", K);
+        PCB_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+        launch_var_scan(c, v, d_jobs, static_cast<int>(jobs.size()), xr);
+        const RankOut& R = *v.rank;
+        k_var_final<<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, d_flags, R.route, v.n_rows, zb, xr,
+                                                  static_cast<uint32_t>(R.cl), R.rcap, v.partials, v.tickets);
+        c.count_launch();
+    }
+    if (any_global) launch_var_global(c, v, d_flags + K, zb, Ag);
     PCB_CUDA(cudaEventSynchronize(c.ev[7]));
     float ms = 0.0f;
     PCB_CUDA(cudaEventElapsedTime(&ms, c.ev[6], c.ev[7]));
-    c.stage_ms[9] = ms;  // variance pass 1 (per-point terms); the rest of [3] is pass 2
+    c.stage_ms[9] = ms;  // variance pass 1 (per-point terms); the rest of [3] is passes 2-3
 }
 
 }  // namespace pcb
