@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libparcop_b200.so")
+# PCB_LIB_PATH selects an alternative in-tree build (kernel experiments)
+LIB_PATH = os.environ.get("PCB_LIB_PATH") or os.path.join(HERE, "libparcop_b200.so")
 
 # Every symbol include/parcop_b200.h declares (tests check the export table).
 SYMBOLS = (

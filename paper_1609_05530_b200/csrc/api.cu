@@ -320,7 +320,7 @@ int pcb_normalized_ranks(pcb_context* ctx, const double* col1, const double* col
         for (int32_t b : bad)
             if (b) throw pcb::Error(PCB_E_DOMAIN, "data matrix: non-finite value");  // pseudo_obs.hpp:36
         DevOut<double> o1(c, u1, n_rows, "u1"), o2(c, u2, n_rows, "u2");
-        pcb::ranks_to_u(c, rb.r.rp, n_rows, off, o1.dev, o2.dev);
+        pcb::ranks_to_u(c, rb.r, n_rows, off, o1.dev, o2.dev);
         o1.finish(c);
         o2.finish(c);
         PCB_CUDA(cudaStreamSynchronize(c.stream));

@@ -143,6 +143,34 @@ __host__ __device__ __forceinline__ uint32_t rank_pos(unsigned long long rp) {
 }
 __host__ __device__ __forceinline__ bool rank_first(unsigned long long rp) { return (rp >> 63) != 0; }
 
+// How a kernel reads the two ranks (r2 = twice the average rank) of a row:
+// blocks the cluster rank path handled ("routed") keep their ranks per
+// receive slot of the rank all-to-all, found through route[row]; all other
+// blocks keep packed ranks by row.
+struct RankRef {
+    const unsigned long long* rp;  // [2][n_rows] by row (blocks not routed)
+    const uint32_t* route;         // [2][n_rows] (owner << 16) | receive slot
+    const uint32_t* r2s;           // [2][nseg][cl][rcap] r2 per slot
+    const uint8_t* routed;         // [nseg] or null
+    uint32_t cl, rcap;
+};
+
+__device__ __forceinline__ uint64_t slot_index(const RankRef& R, int nseg, int col, int m, uint32_t rw) {
+    return ((static_cast<uint64_t>(col) * nseg + m) * R.cl + (rw >> 16)) * R.rcap + (rw & 0xffffu);
+}
+
+__device__ __forceinline__ void rank_pair(const RankRef& R, bool routed, int nseg, int m, uint64_t n_rows,
+                                          uint64_t row, uint32_t& r1, uint32_t& r2) {
+    if (routed) {
+        const uint32_t w1 = R.route[row], w2 = R.route[n_rows + row];
+        r1 = R.r2s[slot_index(R, nseg, 0, m, w1)];
+        r2 = R.r2s[slot_index(R, nseg, 1, m, w2)];
+    } else {
+        r1 = rank_r2(R.rp[row]);
+        r2 = rank_r2(R.rp[n_rows + row]);
+    }
+}
+
 // (u, v) of a point: the caller's pseudo-observations, or exactly
 // normalized_rank_column's value from the packed rank (pseudo_obs.hpp:59-60).
 __device__ __forceinline__ void point_u(const unsigned long long* rp, const double* u1, const double* u2,

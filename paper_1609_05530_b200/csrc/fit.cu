@@ -167,8 +167,7 @@ __global__ void k_init_state(BlockState* st, const Seg* segs, int nseg, const in
 // u only) holds the per-rank transform of the block's size: Phi^-1(u)
 // (Gaussian) or ln(-ln u) (Gumbel), bit-identical to computing it per point.
 template <int FAM, class TO>
-__global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs, int nseg,
-                                               const unsigned long long* __restrict__ rp,
+__global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs, int nseg, RankRef R,
                                                const double* __restrict__ u1, const double* __restrict__ u2,
                                                uint64_t n_rows, TO* __restrict__ T, float2* __restrict__ T32,
                                                const double* __restrict__ gtab, const uint64_t* goff,
@@ -181,10 +180,38 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
     const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);
     const uint32_t base = (tile - S.tile0) * FTILE;
     const double* gt = gtab ? gtab + goff[m] : nullptr;
+    const bool rt = R.routed && R.routed[m];
     double v[2] = {0.0, 0.0};
     constexpr int U = 4;  // points per thread in flight
     for (int k0 = 0; k0 < PPT; k0 += U) {
         double uu[U], ww[U], gx[U], gy[U];
+        uint32_t ra[U], rb[U];
+        if (!u1) {
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+                if (i < S.n) {
+                    const uint64_t row = S.begin + i;
+                    if (rt) {
+                        ra[j] = R.route[row];
+                        rb[j] = R.route[n_rows + row];
+                    } else {
+                        ra[j] = rank_r2(R.rp[row]);
+                        rb[j] = rank_r2(R.rp[n_rows + row]);
+                    }
+                }
+            }
+            if (rt) {
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+                    if (i < S.n) {
+                        ra[j] = R.r2s[slot_index(R, nseg, 0, m, ra[j])];
+                        rb[j] = R.r2s[slot_index(R, nseg, 1, m, rb[j])];
+                    }
+                }
+            }
+        }
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
@@ -194,7 +221,7 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
                     uu[j] = u1[row];
                     ww[j] = u2[row];
                 } else {
-                    const uint32_t r1 = rank_r2(rp[row]), r2 = rank_r2(rp[n_rows + row]);
+                    const uint32_t r1 = ra[j], r2 = rb[j];
                     uu[j] = __dmul_rn(0.5 * static_cast<double>(r1), scale);
                     ww[j] = __dmul_rn(0.5 * static_cast<double>(r2), scale);
                     if (gt) {
@@ -514,11 +541,11 @@ void launch_prepare(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int
                     bool fp32T, float2* T32, const double* gtab, const uint64_t* goff, double* part, unsigned* tick,
                     unsigned* running, int with_fit) {
     if (fp32T)
-        k_prepare<FAM, float2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.rp, io.u1, io.u2, io.n_rows,
+        k_prepare<FAM, float2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.rank->ref(), io.u1, io.u2, io.n_rows,
                                                           static_cast<float2*>(T), nullptr, gtab, goff, part, tick,
                                                           running, with_fit);
     else
-        k_prepare<FAM, double2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.rp, io.u1, io.u2, io.n_rows,
+        k_prepare<FAM, double2><<<tiles, FT, 0, c.stream>>>(st, segs, K, io.rank->ref(), io.u1, io.u2, io.n_rows,
                                                            static_cast<double2*>(T), T32, gtab, goff, part, tick,
                                                            running, with_fit);
     c.count_launch();

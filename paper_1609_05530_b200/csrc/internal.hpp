@@ -96,21 +96,27 @@ struct Ctx {
 //   bit  63    pos is the first position of its tie run
 // The run-start bits of a segment, set at the positions, mark where every
 // tie run begins; the variance finds a run's first position from them.
-// Cluster-ranked blocks also leave the route of their all-to-all (the
-// variance reuses it as a pre-planned, semi-coalesced permutation):
-//   route [2][n_rows] u32 : (owner CTA << 16) | receive slot of each element
+// Ranks of both columns of every block. Blocks ranked by the cluster path
+// ("routed") keep them in the route space of the rank all-to-all:
+//   route [2][n_rows] u32 : (owner CTA << 16) | receive slot of each row
+//   r2s   [2][K][cl][rcap] u32 : twice the average rank, per receive slot
 //   posl  [2][K][cl][rcap] u16 : owner-local sorted position (15 bits) |
-//                               run-start bit, per receive slot
+//                                run-start bit, per receive slot
 //   ocnt  [2][K][cl] u32 : elements each owner received
-//   routed[m] : both columns of block m went through the cluster path
+// and every other block keeps packed ranks by row in rp.
 struct RankOut {
     unsigned long long* rp = nullptr;
     uint32_t* route = nullptr;
+    uint32_t* r2s = nullptr;
     uint16_t* posl = nullptr;
     uint32_t* ocnt = nullptr;
     int cl = 0;
     uint32_t rcap = 0;
-    std::vector<uint8_t> routed;
+    std::vector<uint8_t> routed;  // host copy
+    uint8_t* d_routed = nullptr;  // device copy
+    RankRef ref() const {
+        return RankRef{rp, route, r2s, d_routed, static_cast<uint32_t>(cl), rcap};
+    }
 };
 
 // Ranks both columns of every segment. `bad` (n_seg int32, device) is set
@@ -119,7 +125,7 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
                RankOut& out, int32_t* d_bad);
 
 // u = (0.5*r2) * (1/(n_m+1)), bit-exact to normalized_rank_column
-void ranks_to_u(Ctx& c, const unsigned long long* rp, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
+void ranks_to_u(Ctx& c, const RankOut& R, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
                 double* u2);
 
 // ---------------------------------------------------------------- fit

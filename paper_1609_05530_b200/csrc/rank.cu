@@ -321,18 +321,20 @@ __global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const 
     }
 }
 
-__global__ void k_ranks_to_u(const Seg* segs, int nseg, const unsigned long long* rp, uint64_t n_rows, double* u1,
-                             double* u2) {
+__global__ void k_ranks_to_u(const Seg* segs, int nseg, RankRef R, uint64_t n_rows, double* u1, double* u2) {
     const int m = seg_of_tile(segs, nseg, blockIdx.x);
     const Seg S = segs[m];
     const uint32_t begin = (blockIdx.x - S.tile0) * RTILE;
     const uint32_t end = min(begin + RTILE, S.n);
     const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);  // pseudo_obs.hpp:53
+    const bool rt = R.routed && R.routed[m];
     for (uint32_t i = begin + threadIdx.x; i < end; i += RT) {
         const uint64_t row = S.begin + i;
+        uint32_t r1, r2;
+        rank_pair(R, rt, nseg, m, n_rows, row, r1, r2);
         // pseudo_obs.hpp:59-60: avg = 0.5*((i+1)+(j+1)); u = avg*scale
-        u1[row] = __dmul_rn(0.5 * static_cast<double>(rank_r2(rp[row])), scale);
-        u2[row] = __dmul_rn(0.5 * static_cast<double>(rank_r2(rp[n_rows + row])), scale);
+        u1[row] = __dmul_rn(0.5 * static_cast<double>(r1), scale);
+        u2[row] = __dmul_rn(0.5 * static_cast<double>(r2), scale);
     }
 }
 
@@ -346,20 +348,23 @@ uint32_t tiles_of(uint64_t n) { return static_cast<uint32_t>((n + RTILE - 1) / R
 //   2. value-linear split of [min, max] into CL contiguous value ranges
 //      (one per CTA) x NBL local buckets; every CTA counts what it sends
 //      to each peer; the CL x CL count matrix is read through DSMEM
-//   3. every element is stored (key, row) into its value-range owner's
-//      receive buffer (DSMEM stores)
+//   3. every element's key is stored into its value-range owner's receive
+//      buffer (one 8-byte DSMEM store); route[row] = (owner, receive slot)
 //   4. each owner counting-sorts its elements into NBL local buckets and
 //      ranks every element by counting inside its bucket; lt = elements in
-//      lower value ranges + bucket start + #less
-// HBM traffic: 8 B read + 8 B (packed r2|pos) write per element. A slice
-// whose received count would overflow its buffer (heavily skewed data) or
+//      lower value ranges + bucket start + #less; equal keys are ordered by
+//      receive slot
+//   5. results per receive slot (coalesced): r2 (u32) and the owner-local
+//      sorted position with the run-start bit (u16); consumers read them
+//      through route[row]
+// HBM traffic per element: 8 B read; 4 B route + 4 B r2 + 2 B position
+// written. A slice whose received count would overflow its buffer (heavily
+// skewed data) or
 // a non-finite range falls back to the global path.
 constexpr int CT = 1024;  // threads per cluster CTA
 constexpr int NWARP = CT / 32;
 constexpr int EMAX = 16;         // slice elements per thread (slice <= 16K)
 constexpr int QMAX = 16;         // received elements per thread (RCAP <= QMAX * CT)
-constexpr int kIdxBits = 18;     // row within the block (< 2^18) | local bucket in the high bits
-constexpr uint32_t kIdxMask = (1u << kIdxBits) - 1u;
 constexpr int kMaxCluster = 16;
 constexpr size_t kSmemLimit = 227 * 1024 - 8192;  // leave room for static shared memory
 
@@ -381,10 +386,14 @@ inline bool getenv_flag(const char* name) {
     return v && v[0] && v[0] != '0';
 }
 
+__host__ __device__ inline uint32_t slice_of(uint64_t n, int cl) {
+    return static_cast<uint32_t>(((n + cl - 1) / cl + 31) & ~31ull);
+}
+
 inline ClusterPlan plan_for(uint64_t nmax, int cl) {
     ClusterPlan p;
     p.cl = cl;
-    p.s = static_cast<uint32_t>((nmax + cl - 1) / cl);
+    p.s = slice_of(nmax, cl);
     const uint32_t slack = std::max<uint32_t>(256u, static_cast<uint32_t>(6.0 * std::sqrt(static_cast<double>(p.s))));
     p.rcap = (p.s + slack + 31u) & ~31u;
     uint32_t lg = 1;
@@ -402,7 +411,7 @@ inline ClusterPlan plan_cluster(uint64_t nmax) {
         if (forced && cl != forced) continue;
         ClusterPlan p = plan_for(nmax, cl);
         if (p.rcap <= static_cast<uint32_t>(QMAX * CT) && p.rcap < 32768 && p.smem <= kSmemLimit && p.s <= static_cast<uint32_t>(EMAX * CT) &&
-            nmax <= kIdxMask && (p.lg_nbl + kIdxBits) <= 32 && (static_cast<uint64_t>(cl) << p.lg_nbl) <= 65536)
+            (static_cast<uint64_t>(cl) << p.lg_nbl) <= 65536)
             return p;
     }
     return ClusterPlan{};
@@ -455,7 +464,8 @@ __device__ void block_scan_excl_u16(uint32_t* cw, uint16_t* start, uint32_t n, u
 
 __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, const double* c0, const double* c1,
                                                        uint64_t n_rows, unsigned long long* rp, uint32_t* route,
-                                                       uint16_t* posl_g, uint32_t* ocnt, uint32_t K, int32_t* fb,
+                                                       uint32_t* r2s_g, uint16_t* posl_g, uint32_t* ocnt, uint32_t K,
+                                                       int32_t* fb,
                                                        int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
                                                        unsigned long long* prof) {
     namespace cg = cooperative_groups;
@@ -472,15 +482,15 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     const uint32_t jid = blockIdx.x / CL;
     const ClusterJob J = jobs[jid];
     const double* x = (J.col ? c1 : c0) + J.begin;
-    const uint32_t S = (J.n + CL - 1) / CL;
+    const uint32_t S = slice_of(J.n, CL);  // 32-aligned slices: a warp's 32 rows share one send pass
     const uint32_t a = min(J.n, r * S), e = min(J.n, a + S);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t NBL = 1u << lg_nbl;
 
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* recv_key = reinterpret_cast<unsigned long long*>(smem);
-    uint32_t* recv_idx = reinterpret_cast<uint32_t*>(recv_key + RCAP);
-    uint32_t* lhw = recv_idx + RCAP;                            // NBL u16 counts -> cursors, two per word
+    uint32_t* outw = reinterpret_cast<uint32_t*>(recv_key + RCAP);  // local bucket, then the slot's result
+    uint32_t* lhw = outw + RCAP;                            // NBL u16 counts -> cursors, two per word
     uint16_t* lhs = reinterpret_cast<uint16_t*>(lhw + NBL / 2);  // NBL+1 u16 starts (+1 pad)
     uint16_t* perm = lhs + NBL + 2;
 
@@ -650,59 +660,54 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     for (int q = tid; q < NWARP * CL; q += CT) s_wc[q / CL][q % CL] += s_off[q % CL];
     __syncthreads();
 
-    // ---- 3. scatter (key, local bucket | row) to the owners (DSMEM stores)
-    const uint32_t lmask = NBL - 1u;
+    // ---- 3. scatter keys to the owners (one 8-byte DSMEM store per element).
+    // The owner never needs the row: its outputs are written per receive slot
+    // and the row finds them through route[row] = (owner, slot).
 #pragma unroll
     for (int k = 0; k < EMAX; ++k) {
         const uint32_t i = a + k * CT + tid;
         if (i < e) {
             const unsigned long long kk = order_key(x[i]);
-            const uint32_t b = (bk[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
-            const uint32_t d = b >> lg_nbl;
+            const uint32_t d = ((bk[k >> 1] >> ((k & 1) * 16)) & 0xffffu) >> lg_nbl;
             const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
-            route[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = (d << 16) | slot;  // owner, receive slot
+            route[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = (d << 16) | slot;
             *cluster.map_shared_rank(recv_key + slot, d) = kk;
-            *cluster.map_shared_rank(recv_idx + slot, d) = ((b & lmask) << kIdxBits) | i;
         }
     }
     cluster.sync();  // every receive buffer is complete; no DSMEM access after this point
     mark(3);
 
-    // ---- 4. local counting sort into NBL buckets
+    // ---- 4. local counting sort into NBL buckets (the sender's bucket map,
+    // recomputed from the key)
     const uint32_t T = s_total, base = s_base;
+    const uint32_t lmask = NBL - 1u;
     for (uint32_t q = tid; q < NBL / 2; q += CT) lhw[q] = 0u;
     __syncthreads();
     for (uint32_t j = tid; j < T; j += CT) {
-        const uint32_t lb = recv_idx[j] >> kIdxBits;
+        const uint32_t lb = cbucket(recv_key[j], hm, scale, nbtot) & lmask;
+        outw[j] = lb;
         atomicAdd(lhw + (lb >> 1), 1u << ((lb & 1) * 16));
     }
     __syncthreads();
     block_scan_excl_u16(lhw, lhs, NBL, s_w);  // counts < 2^16: a bucket never exceeds RCAP < 65535
     for (uint32_t j = tid; j < T; j += CT) {
-        const uint32_t lb = recv_idx[j] >> kIdxBits, sh = (lb & 1) * 16;
+        const uint32_t lb = outw[j], sh = (lb & 1) * 16;
         const uint32_t slot = (atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu;
         perm[slot] = static_cast<uint16_t>(j);
     }
     __syncthreads();
 
     mark(4);
-    // ---- 5. rank inside each bucket; write packed (r2 | pos | run-start)
-    unsigned long long* out = rp + static_cast<uint64_t>(J.col) * n_rows + J.begin;
-    // this owner's region of the route space: local sorted position (15 bits) | run-start bit
-    uint16_t* po = posl_g + ((static_cast<uint64_t>(J.col) * K + J.seg) * CL + r) * RCAP;
-    if (tid == 0) ocnt[(static_cast<uint64_t>(J.col) * K + J.seg) * CL + r] = T;
+    // ---- 5. rank inside each bucket. Equal keys are ordered by receive slot
+    // (any fixed order of a tie run gives the same average rank and the same
+    // run start, which is all any output depends on). Per slot:
+    //   outw = (local r2 << 16) | local sorted position | run-start bit
     // walk the elements in bucket order: a warp's lanes mostly share buckets, so
-    // the bucket-mate loads are shared-memory broadcasts. (slot, local position)
-    // pairs stay in registers until perm is free, then go out in slot order.
-    uint32_t keep[QMAX];
-#pragma unroll
-    for (int k = 0; k < QMAX; ++k) {
-        const uint32_t qq = tid + k * CT;
-        if (qq >= T) break;
+    // the bucket-mate loads are shared-memory broadcasts
+    for (uint32_t qq = tid; qq < T; qq += CT) {
         const uint32_t j = perm[qq];
         const unsigned long long kv = recv_key[j];
-        const uint32_t id = recv_idx[j];  // (local bucket << kIdxBits) | row: same bucket => compares as row
-        const uint32_t lb = id >> kIdxBits;
+        const uint32_t lb = outw[j];
         const uint32_t s0 = lhs[lb], s1 = lhs[lb + 1];
         uint32_t less = 0, same = 0, before = 0;
 #pragma unroll 1
@@ -712,20 +717,19 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
             less += kq < kv;
             const bool eqk = kq == kv;
             same += eqk;
-            before += eqk && recv_idx[o] < id;
+            before += eqk && o < j;
         }
-        const uint32_t lt = base + s0 + less;
-        out[id & kIdxMask] = pack_rank(2u * lt + same + 1u, lt + before, before == 0);
-        keep[k] = (j << 16) | (lt + before - base) | (before == 0 ? 0x8000u : 0u);
-    }
-    __syncthreads();  // perm is free
-#pragma unroll
-    for (int k = 0; k < QMAX; ++k) {
-        if (tid + k * CT >= T) break;
-        perm[keep[k] >> 16] = static_cast<uint16_t>(keep[k] & 0xffffu);
+        const uint32_t llt = s0 + less;  // < T <= 16384, so local r2 = 2*llt + same + 1 <= 2T < 2^16
+        outw[j] = ((2u * llt + same + 1u) << 16) | (llt + before) | (before == 0 ? 0x8000u : 0u);
     }
     __syncthreads();
-    for (uint32_t j = tid; j < T; j += CT) po[j] = perm[j];
+    const uint64_t reg = ((static_cast<uint64_t>(J.col) * K + J.seg) * CL + r) * RCAP;
+    if (tid == 0) ocnt[(static_cast<uint64_t>(J.col) * K + J.seg) * CL + r] = T;
+    for (uint32_t j = tid; j < T; j += CT) {  // coalesced, in slot order
+        const uint32_t w = outw[j];
+        r2s_g[reg + j] = 2u * base + (w >> 16);
+        posl_g[reg + j] = static_cast<uint16_t>(w & 0xffffu);
+    }
     mark(5);
 }
 
@@ -751,7 +755,8 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
         prof = c.ws.get_t<unsigned long long>("rank.prof", 8);
         PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
     }
-    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, out.rp, out.route, out.posl, out.ocnt,
+    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, out.rp, out.route, out.r2s, out.posl,
+                                out.ocnt,
                                 njobs / 2, fb, bad, p.cl, p.rcap, p.lg_nbl, prof));
     if (prof) {
         unsigned long long h[8];
@@ -896,6 +901,43 @@ void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64
     }
 }
 
+// By-row packed ranks of a cluster-ranked column (blocks the routed variance
+// does not take): rp[row] = (r2, owner base + local position, run start).
+__global__ void k_route_to_rows(const ClusterJob* jobs, const uint32_t* list, uint64_t n_rows, uint32_t K, int CL,
+                                uint32_t RCAP, const uint32_t* route, const uint32_t* r2s, const uint16_t* posl,
+                                const uint32_t* ocnt, unsigned long long* rp) {
+    const ClusterJob J = jobs[list[blockIdx.y]];
+    __shared__ uint32_t s_base[kMaxCluster];
+    const uint64_t cm = static_cast<uint64_t>(J.col) * K + J.seg;
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int d = 0; d < CL; ++d) {
+            s_base[d] = run;
+            run += ocnt[cm * CL + d];
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < J.n; i += gridDim.x * blockDim.x) {
+        const uint64_t row = static_cast<uint64_t>(J.col) * n_rows + J.begin + i;
+        const uint32_t w = route[row], d = w >> 16;
+        const uint64_t idx = (cm * CL + d) * RCAP + (w & 0xffffu);
+        const uint32_t pv = posl[idx];
+        rp[row] = pack_rank(r2s[idx], s_base[d] + (pv & 0x7fffu), (pv & 0x8000u) != 0);
+    }
+}
+
+void route_to_rows(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, const std::vector<uint32_t>& list,
+                   const std::vector<uint64_t>& off, uint64_t n_rows, RankOut& out) {
+    auto* d_list = c.ws.get_t<uint32_t>("rank.convert", list.size());
+    PCB_CUDA(cudaMemcpyAsync(d_list, list.data(), list.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c.stream));
+    uint64_t nmax = 0;
+    for (size_t m = 0; m + 1 < off.size(); ++m) nmax = std::max<uint64_t>(nmax, off[m + 1] - off[m]);
+    const dim3 grid(static_cast<unsigned>(std::min<uint64_t>(64, (nmax + 255) / 256)), static_cast<unsigned>(list.size()));
+    k_route_to_rows<<<grid, 256, 0, c.stream>>>(jobs, d_list, n_rows, static_cast<uint32_t>(off.size() - 1), p.cl,
+                                                p.rcap, out.route, out.r2s, out.posl, out.ocnt, out.rp);
+    c.count_launch();
+}
+
 }  // namespace
 
 void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_rows, const std::vector<uint64_t>& off,
@@ -924,27 +966,38 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
         PCB_CUDA(cudaMemsetAsync(fb, 0, njobs * sizeof(int32_t), c.stream));
         out.cl = plan.cl;
         out.rcap = plan.rcap;
+        const size_t nslot = static_cast<size_t>(njobs) * plan.cl * plan.rcap;
         out.route = c.ws.get_t<uint32_t>("rank.route", 2 * n_rows);
-        out.posl = c.ws.get_t<uint16_t>("rank.posl", static_cast<size_t>(njobs) * plan.cl * plan.rcap);
+        out.r2s = c.ws.get_t<uint32_t>("rank.r2s", nslot);
+        out.posl = c.ws.get_t<uint16_t>("rank.posl", nslot);
         out.ocnt = c.ws.get_t<uint32_t>("rank.ocnt", static_cast<size_t>(njobs) * plan.cl);
         launch_rank_cluster(c, plan, jobs, njobs, d_col1, d_col2, n_rows, out, fb, d_bad);
         std::vector<int32_t> hfb(njobs);
         PCB_CUDA(cudaMemcpyAsync(hfb.data(), fb, njobs * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
         PCB_CUDA(cudaStreamSynchronize(c.stream));
-        out.routed.assign(K, 1);
+        // a block is routed when both columns went through the cluster path;
+        // cluster-ranked columns of other blocks get their by-row ranks rebuilt
+        const bool force_rows = getenv_flag("PCB_VAR_GLOBAL");
+        out.routed.assign(K, force_rows ? 0 : 1);
         for (uint32_t j = 0; j < njobs; ++j) {
             if (hfb[j]) out.routed[j % K] = 0;
             if (hfb[j] == 1) fallback.push_back(j);
         }
+        std::vector<uint32_t> convert;
+        for (uint32_t j = 0; j < njobs; ++j)
+            if (hfb[j] == 0 && !out.routed[j % K]) convert.push_back(j);
+        if (!convert.empty()) route_to_rows(c, plan, jobs, convert, off, n_rows, out);
     } else {
         out.cl = 0;
         out.routed.assign(K, 0);
         for (uint32_t j = 0; j < 2 * K; ++j) fallback.push_back(j);
     }
+    out.d_routed = c.ws.get_t<uint8_t>("rank.routed", K);
+    PCB_CUDA(cudaMemcpyAsync(out.d_routed, out.routed.data(), K, cudaMemcpyHostToDevice, c.stream));
     run_ranks_global(c, d_col1, d_col2, n_rows, off, fallback, out, d_bad);
 }
 
-void ranks_to_u(Ctx& c, const unsigned long long* rp, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
+void ranks_to_u(Ctx& c, const RankOut& R, uint64_t n_rows, const std::vector<uint64_t>& off, double* u1,
                 double* u2) {
     const size_t K = off.size() - 1;
     std::vector<Seg> segs(K);
@@ -956,7 +1009,7 @@ void ranks_to_u(Ctx& c, const unsigned long long* rp, uint64_t n_rows, const std
     if (tiles == 0) return;
     auto* d_segs = c.ws.get_t<Seg>("u.segs", K);
     PCB_CUDA(cudaMemcpyAsync(d_segs, segs.data(), K * sizeof(Seg), cudaMemcpyHostToDevice, c.stream));
-    k_ranks_to_u<<<tiles, RT, 0, c.stream>>>(d_segs, static_cast<int>(K), rp, n_rows, u1, u2);
+    k_ranks_to_u<<<tiles, RT, 0, c.stream>>>(d_segs, static_cast<int>(K), R.ref(), n_rows, u1, u2);
     c.count_launch();
 }
 

@@ -83,14 +83,12 @@ __device__ __forceinline__ bool flag_of(double x) { return (__double_as_longlong
 
 // ------------------------------------------------------------ pass 1
 template <int FAM>
-__global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* segs, int nseg,
-                                                 const unsigned long long* __restrict__ rp,
+__global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* segs, int nseg, RankRef R,
                                                  const double* __restrict__ u1, const double* __restrict__ u2,
                                                  const double2* __restrict__ T64, const double* __restrict__ gtab,
                                                  const uint64_t* goff, uint64_t n_rows, double* __restrict__ zb,
-                                                 double* __restrict__ Ag, const uint8_t* __restrict__ routed,
-                                                 const uint32_t* __restrict__ route, double* __restrict__ xr,
-                                                 uint32_t CL, uint32_t RCAP, double* partials, unsigned* tickets) {
+                                                 double* __restrict__ Ag, double* __restrict__ xr, double* partials,
+                                                 unsigned* tickets) {
     const uint32_t tile = blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
@@ -100,14 +98,14 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
     const uint32_t base = (tile - S.tile0) * FTILE;
     const double* gt = gtab ? gtab + goff[m] : nullptr;
     const bool has_t = gt || T64;
-    const bool rt = routed && routed[m];
-    double* x1 = rt ? xr + static_cast<uint64_t>(m) * CL * RCAP : nullptr;
-    double* x2 = rt ? xr + (static_cast<uint64_t>(nseg) + m) * CL * RCAP : nullptr;
+    const bool rt = R.routed && R.routed[m];
+    const uint64_t c1 = rt ? slot_index(R, nseg, 0, m, 0u) : 0, c2 = rt ? slot_index(R, nseg, 1, m, 0u) : 0;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     constexpr int U = 2;  // points per thread in flight
     for (int k0 = 0; k0 < PPT; k0 += U) {
-        unsigned long long p1[U], p2[U];
-        uint32_t r1[U], r2[U];
+        unsigned long long p1[U], p2[U];  // packed ranks (by-row blocks)
+        uint32_t w1[U], w2[U];            // route words (routed blocks)
+        uint32_t q1[U], q2[U];            // r2
         double2 tt[U];
         double uu[U], ww[U];
 #pragma unroll
@@ -115,17 +113,30 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
             const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
             if (i < S.n) {
                 const uint64_t row = S.begin + i;
-                p1[j] = rp[row];
-                p2[j] = rp[n_rows + row];
+                if (rt) {
+                    w1[j] = R.route[row];
+                    w2[j] = R.route[n_rows + row];
+                } else {
+                    p1[j] = R.rp[row];
+                    p2[j] = R.rp[n_rows + row];
+                }
                 if (u1) {
                     uu[j] = u1[row];
                     ww[j] = u2[row];
                 }
                 if (T64) tt[j] = T64[row];
-                if (rt) {
-                    r1[j] = route[row];
-                    r2[j] = route[n_rows + row];
-                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            if (i >= S.n) continue;
+            if (!rt) {
+                q1[j] = rank_r2(p1[j]);
+                q2[j] = rank_r2(p2[j]);
+            } else if (!u1) {
+                q1[j] = R.r2s[c1 + (w1[j] >> 16) * R.rcap + (w1[j] & 0xffffu)];
+                q2[j] = R.r2s[c2 + (w2[j] >> 16) * R.rcap + (w2[j] & 0xffffu)];
             }
         }
 #pragma unroll
@@ -133,16 +144,16 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
             const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
             if (i >= S.n) continue;
             const uint64_t row = S.begin + i;
-            double u = u1 ? uu[j] : __dmul_rn(0.5 * static_cast<double>(rank_r2(p1[j])), scale);
-            double w = u1 ? ww[j] : __dmul_rn(0.5 * static_cast<double>(rank_r2(p2[j])), scale);
+            double u = u1 ? uu[j] : __dmul_rn(0.5 * static_cast<double>(q1[j]), scale);
+            double w = u1 ? ww[j] : __dmul_rn(0.5 * static_cast<double>(q2[j]), scale);
             u = clamp_unit(u);
             w = clamp_unit(w);
-            if (gt) tt[j] = make_double2(gt[rank_r2(p1[j])], gt[rank_r2(p2[j])]);
+            if (gt) tt[j] = make_double2(gt[q1[j]], gt[q2[j]]);
             const PointFull p = eval_point<FAM>(th, u, w, tt[j], has_t);
             zb[row] = p.score;
             if (rt) {  // cross_j to (owner, slot) of the rank stage's route
-                x1[(r1[j] >> 16) * RCAP + (r1[j] & 0xffffu)] = p.cross1;
-                x2[(r2[j] >> 16) * RCAP + (r2[j] & 0xffffu)] = p.cross2;
+                xr[c1 + (w1[j] >> 16) * R.rcap + (w1[j] & 0xffffu)] = p.cross1;
+                xr[c2 + (w2[j] >> 16) * R.rcap + (w2[j] & 0xffffu)] = p.cross2;
             } else {  // cross_j to its sorted position, run-start flag beside it
                 const uint64_t q1 = S.begin + rank_pos(p1[j]), q2 = n_rows + S.begin + rank_pos(p2[j]);
                 Ag[q1] = with_flag(p.cross1, rank_first(p1[j]));
@@ -176,6 +187,13 @@ __device__ __forceinline__ double finish_sigma2(BlockState& s, double zz, double
 // ------------------------------------------------------------ pass 2 (routed)
 // Cluster of the block's CL owners; CTA r holds owner r's slots. Per column:
 // place, suffix-scan with carry from owners above, W per slot in place.
+// Thread t handles slots t + k*VT (k < JMAX; the rank plan keeps RCAP <=
+// JMAX*VT), so a slot's local position stays in registers from the place
+// step to the W step. The run-start flag rides in the LSB of the placed
+// cross value and becomes a bitmap in the scan's first pass.
+constexpr int JMAX = 16;
+constexpr int JH = 4;  // loads in flight per thread in the place step
+
 __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const int* seg_list, int nseg,
                                                    const Seg* segs, const uint16_t* __restrict__ posl,
                                                    const uint32_t* __restrict__ ocnt, double* __restrict__ xr, int CL,
@@ -192,13 +210,13 @@ __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const 
     const int r = static_cast<int>(cluster.block_rank());
     const int m = seg_list[blockIdx.x / CL];
     if (st[m].status != kConverged) return;  // uniform across the cluster, before any DSMEM access
-    const double nd = static_cast<double>(segs[m].n);
+    const double inv_n = 1.0 / static_cast<double>(segs[m].n);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
     extern __shared__ __align__(16) unsigned char smem[];
-    double* A = reinterpret_cast<double*>(smem);                 // owner-local sorted positions
-    uint32_t* bits = reinterpret_cast<uint32_t*>(A + RCAP);      // run-start bit per position
-    __shared__ double s_tot;
+    double* A = reinterpret_cast<double*>(smem);             // owner-local sorted positions
+    uint32_t* bits = reinterpret_cast<uint32_t*>(A + RCAP);  // run-start bit per position
+    __shared__ double s_tot, s_carry;
     __shared__ double s_wt[VNW], s_wo[VNW];
 
     for (int col = 0; col < 2; ++col) {
@@ -209,36 +227,40 @@ __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const 
         const uint16_t* P = posl + reg;
         cluster.sync();  // the previous column is finished everywhere (s_tot, A, bits reusable)
         mark(0);
-        for (uint32_t q = tid; q <= T / 32; q += VT) bits[q] = 0u;
-        __syncthreads();
-        // place: coalesced slot loads, random shared-memory stores
-        for (uint32_t j0 = tid; j0 < T; j0 += VT * 4) {
-            double x[4];
-            uint32_t pv[4];
+        // place: coalesced slot loads (JH in flight), random shared-memory stores
+        uint32_t pk[JMAX / 2];  // this thread's local positions, two per register
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t j = j0 + u * VT;
+        for (int h = 0; h < JMAX; h += JH) {
+            double x[JH];
+            uint32_t pv[JH];
+#pragma unroll
+            for (int k = 0; k < JH; ++k) {
+                const uint32_t j = tid + (h + k) * VT;
                 if (j < T) {
-                    x[u] = X[j];
-                    pv[u] = P[j];
+                    x[k] = X[j];
+                    pv[k] = P[j];
+                } else {
+                    pv[k] = 0xffffu;
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t j = j0 + u * VT;
-                if (j >= T) continue;
-                const uint32_t p = pv[u] & 0x7fffu;
-                A[p] = x[u];
-                if (pv[u] & 0x8000u) atomicOr(bits + (p >> 5), 1u << (p & 31));
+            for (int k = 0; k < JH; ++k) {
+                if (pv[k] != 0xffffu) A[pv[k] & 0x7fffu] = with_flag(x[k], (pv[k] & 0x8000u) != 0);
+                if (k & 1) pk[(h + k) >> 1] = pv[k - 1] | (pv[k] << 16);
             }
         }
         __syncthreads();
         mark(1);
-        // warp w scans the contiguous positions [w*WL, (w+1)*WL)
+        // warp w scans the contiguous positions [w*WL, (w+1)*WL) (32-aligned)
         const uint32_t WL = ((T + VNW - 1) / VNW + 31) & ~31u;
         const uint32_t w0 = min(T, wid * WL), w1 = min(T, w0 + WL);
         double wsum = 0.0;
-        for (uint32_t q = w0 + lane; q < w1; q += 32) wsum += A[q];
+        for (uint32_t q = w0 + lane; q - lane < w1; q += 32) {
+            const double v = q < w1 ? A[q] : 0.0;
+            const unsigned fl = __ballot_sync(0xffffffffu, q < w1 && flag_of(v));
+            if (lane == 0) bits[q >> 5] = fl;
+            wsum += v;
+        }
         wsum = warp_sum(wsum);
         if (lane == 0) s_wt[wid] = wsum;
         __syncthreads();
@@ -253,8 +275,13 @@ __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const 
             if (lane == 0) s_tot = x;
         }
         cluster.sync();  // owner totals published
-        double carry = s_wo[wid];
-        for (int q = r + 1; q < CL; ++q) carry += *cluster.map_shared_rank(&s_tot, q);  // owners above
+        if (tid == 0) {  // owners above, in fixed order
+            double c = 0.0;
+            for (int q = r + 1; q < CL; ++q) c += *cluster.map_shared_rank(&s_tot, q);
+            s_carry = c;
+        }
+        __syncthreads();
+        double carry = s_wo[wid] + s_carry;
         for (uint32_t t = (w1 - w0 + 31) / 32; t-- > 0;) {
             const uint32_t q = w0 + t * 32 + lane;
             double x = q < w1 ? A[q] : 0.0;
@@ -269,8 +296,11 @@ __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const 
         __syncthreads();
         mark(2);
         // W_j per slot: suffix sum at the start of the slot's tie run (owner-local)
-        for (uint32_t j = tid; j < T; j += VT) {
-            const uint32_t pv = P[j];
+#pragma unroll
+        for (int k = 0; k < JMAX; ++k) {
+            const uint32_t j = tid + k * VT;
+            if (j >= T) break;
+            const uint32_t pv = (pk[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
             uint32_t q = pv & 0x7fffu;
             if (!(pv & 0x8000u)) {
                 uint32_t t = q - 1;  // position 0 of an owner always starts a run
@@ -283,7 +313,7 @@ __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const 
                     t = (t & ~31u) - 1;
                 }
             }
-            X[j] = (A[q] - cj) / nd;
+            X[j] = (A[q] - cj) * inv_n;
         }
         mark(3);
     }
@@ -291,17 +321,17 @@ __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const 
 }
 
 // z = score + W_1 + W_2 per row (through the route), sum z^2 -> sigma2
-__global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* segs, int nseg,
-                                                 const uint8_t* __restrict__ routed,
-                                                 const uint32_t* __restrict__ route, uint64_t n_rows,
-                                                 const double* __restrict__ zb, const double* __restrict__ xr,
-                                                 uint32_t CL, uint32_t RCAP, double* partials, unsigned* tickets) {
+__global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* segs, int nseg, RankRef R,
+                                                 uint64_t n_rows, const double* __restrict__ zb,
+                                                 const double* __restrict__ xr, double* partials, unsigned* tickets) {
     const uint32_t tile = blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
-    if (!routed[m] || st[m].status != kConverged) return;
-    const double* x1 = xr + static_cast<uint64_t>(m) * CL * RCAP;
-    const double* x2 = xr + (static_cast<uint64_t>(nseg) + m) * CL * RCAP;
+    if (!R.routed[m] || st[m].status != kConverged) return;
+    const uint32_t RCAP = R.rcap;
+    const uint32_t* route = R.route;
+    const double* x1 = xr + slot_index(R, nseg, 0, m, 0u);
+    const double* x2 = xr + slot_index(R, nseg, 1, m, 0u);
     const uint32_t base = (tile - S.tile0) * FTILE;
     double v[1] = {0.0};
     constexpr int U = 4;
@@ -453,12 +483,10 @@ __global__ void __launch_bounds__(FT) k_var_gather_g(BlockState* st, const Seg* 
 }
 
 template <int FAM>
-void launch_var_point(Ctx& c, const VarIO& v, double* zb, double* Ag, const uint8_t* d_routed, double* xr) {
+void launch_var_point(Ctx& c, const VarIO& v, double* zb, double* Ag, double* xr) {
     const int K = static_cast<int>(v.off->size() - 1);
-    const RankOut* R = v.rank;
-    k_var_point<FAM><<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, v.rp, v.u1, v.u2, v.T64, v.gtab, v.goff,
-                                                   v.n_rows, zb, Ag, d_routed, R ? R->route : nullptr, xr,
-                                                   R ? R->cl : 0, R ? R->rcap : 0, v.partials, v.tickets);
+    k_var_point<FAM><<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, v.rank->ref(), v.u1, v.u2, v.T64, v.gtab,
+                                                   v.goff, v.n_rows, zb, Ag, xr, v.partials, v.tickets);
     c.count_launch();
 }
 
@@ -517,44 +545,37 @@ void launch_var_global(Ctx& c, const VarIO& v, const uint8_t* use, double* zb, d
 void run_variance(Ctx& c, const VarIO& v) {
     const std::vector<uint64_t>& off = *v.off;
     const int K = static_cast<int>(off.size() - 1);
+    const RankOut& R = *v.rank;
     auto* zb = c.ws.get_t<double>("var.z", v.n_rows);
-    // which blocks take the routed path (the rank stage's cluster route)
-    std::vector<uint8_t> routed(K, 0);
-    const char* vg = std::getenv("PCB_VAR_GLOBAL");
-    const bool force_global = vg && vg[0] && vg[0] != '0';
+    // routed blocks (both columns ranked by the cluster path) reuse its route;
+    // the others go through sorted-order arrays in global memory
     int nrouted = 0;
-    if (v.rank && v.rank->cl > 0 && !force_global && static_cast<int>(v.rank->routed.size()) == K)
-        for (int m = 0; m < K; ++m) nrouted += (routed[m] = v.rank->routed[m]);
-    const bool any_global = nrouted < K;
-    double* Ag = any_global ? c.ws.get_t<double>("var.A", 2 * v.n_rows) : nullptr;
-    double* xr = nrouted ? c.ws.get_t<double>("var.xr", 2 * static_cast<size_t>(K) * v.rank->cl * v.rank->rcap)
-                         : nullptr;
-    uint8_t* d_flags = c.ws.get_t<uint8_t>("var.flags", 2 * static_cast<size_t>(K));  // [routed | global]
-    std::vector<uint8_t> hflags(2 * K);
-    for (int m = 0; m < K; ++m) {
-        hflags[m] = routed[m];
-        hflags[K + m] = !routed[m];
-    }
-    PCB_CUDA(cudaMemcpyAsync(d_flags, hflags.data(), 2 * K, cudaMemcpyHostToDevice, c.stream));
-    const uint8_t* d_routed = nrouted ? d_flags : nullptr;
+    for (int m = 0; m < K; ++m) nrouted += R.routed.size() == static_cast<size_t>(K) && R.routed[m];
+    double* Ag = nrouted < K ? c.ws.get_t<double>("var.A", 2 * v.n_rows) : nullptr;
+    double* xr = nrouted ? c.ws.get_t<double>("var.xr", 2 * static_cast<size_t>(K) * R.cl * R.rcap) : nullptr;
     PCB_CUDA(cudaEventRecord(c.ev[6], c.stream));
-    if (v.family == kGaussian) launch_var_point<kGaussian>(c, v, zb, Ag, d_routed, xr);
-    else if (v.family == kFrank) launch_var_point<kFrank>(c, v, zb, Ag, d_routed, xr);
-    else launch_var_point<kGumbel>(c, v, zb, Ag, d_routed, xr);
+    if (v.family == kGaussian) launch_var_point<kGaussian>(c, v, zb, Ag, xr);
+    else if (v.family == kFrank) launch_var_point<kFrank>(c, v, zb, Ag, xr);
+    else launch_var_point<kGumbel>(c, v, zb, Ag, xr);
     PCB_CUDA(cudaEventRecord(c.ev[7], c.stream));
     if (nrouted) {
         std::vector<int> jobs;
         for (int m = 0; m < K; ++m)
-            if (routed[m]) jobs.push_back(m);
+            if (R.routed[m]) jobs.push_back(m);
         int* d_jobs = c.ws.get_t<int>("var.jobs", K);
         PCB_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
         launch_var_scan(c, v, d_jobs, static_cast<int>(jobs.size()), xr);
-        const RankOut& R = *v.rank;
-        k_var_final<<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, d_flags, R.route, v.n_rows, zb, xr,
-                                                  static_cast<uint32_t>(R.cl), R.rcap, v.partials, v.tickets);
+        k_var_final<<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, R.ref(), v.n_rows, zb, xr, v.partials,
+                                                  v.tickets);
         c.count_launch();
     }
-    if (any_global) launch_var_global(c, v, d_flags + K, zb, Ag);
+    if (nrouted < K) {
+        std::vector<uint8_t> use(K);
+        for (int m = 0; m < K; ++m) use[m] = !(R.routed.size() == static_cast<size_t>(K) && R.routed[m]);
+        uint8_t* d_use = c.ws.get_t<uint8_t>("var.use", K);
+        PCB_CUDA(cudaMemcpyAsync(d_use, use.data(), K, cudaMemcpyHostToDevice, c.stream));
+        launch_var_global(c, v, d_use, zb, Ag);
+    }
     PCB_CUDA(cudaEventSynchronize(c.ev[7]));
     float ms = 0.0f;
     PCB_CUDA(cudaEventElapsedTime(&ms, c.ev[6], c.ev[7]));
