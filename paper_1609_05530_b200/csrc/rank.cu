@@ -494,6 +494,37 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     uint16_t* lhs = reinterpret_cast<uint16_t*>(lhw + NBL / 2);  // NBL+1 u16 starts (+1 pad)
     uint16_t* perm = lhs + NBL + 2;
 
+    // the slice is staged into the (not yet used) receive buffer by one bulk
+    // async copy; the sample and the cluster-wide extremes overlap it
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const uint64_t g_lo = reinterpret_cast<uint64_t>(x + a) & ~15ull;
+    const uint32_t x_off = static_cast<uint32_t>((reinterpret_cast<uint64_t>(x + a) - g_lo) >> 3);
+    const uint64_t g_hi = (reinterpret_cast<uint64_t>(x + e) + 15ull) & ~15ull;
+    const bool staged = e > a;
+    const double* xs = reinterpret_cast<const double*>(smem) + x_off - a;  // xs[i] == x[i] for i in [a, e)
+    if (tid == 0 && staged) {
+        const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
+        const uint32_t bytes = static_cast<uint32_t>(g_hi - g_lo);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+            "l"(g_lo), "r"(bytes), "r"(mb)
+            : "memory");
+    }
+    auto wait_slice = [&]() {
+        if (!staged) return;
+        const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+            "@!p bra WAIT_%=;\n}" ::"r"(mb)
+            : "memory");
+    };
+
     __shared__ unsigned long long s_k[2][NWARP];
     __shared__ unsigned long long s_rmin, s_rmax, s_gmin, s_gmax;  // s_rmin/s_rmax are read by peers
     __shared__ int s_bad, s_gbad, s_over;
@@ -525,13 +556,18 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
             s_k[1][wid] = kmx;
         }
         __syncthreads();
-        if (tid == 0) {
-            for (int w = 1; w < NWARP; ++w) {
-                kmn = min(kmn, s_k[0][w]);
-                kmx = max(kmx, s_k[1][w]);
+        if (wid == 0) {
+            kmn = s_k[0][lane];
+            kmx = s_k[1][lane];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+                kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
             }
-            s_rmin = kmn;
-            s_rmax = kmx;
+            if (lane == 0) {
+                s_rmin = kmn;
+                s_rmax = kmx;
+            }
         }
     };
     auto cluster_extremes = [&]() {
@@ -572,6 +608,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     const double scale = static_cast<double>(nbtot) / (0.5 * vmax - hm);
     const bool constant = s_gmin == s_gmax;
     if (constant || !(isfinite(scale) && scale > 0.0 && isfinite(hm))) {
+        wait_slice();  // no CTA exits with its bulk copy in flight
         if (constant && !isfinite(vmin)) {
             if (r == 0 && tid == 0) {
                 bad[J.seg] = 1;
@@ -594,11 +631,12 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
 #pragma unroll
     for (int k = 0; k < (EMAX + 1) / 2; ++k) bk[k] = 0u;
     bool fin = true;
+    wait_slice();  // the mbarrier was initialised before the first __syncthreads
 #pragma unroll
     for (int k = 0; k < EMAX; ++k) {
         const uint32_t i = a + k * CT + tid;
         if (i < e) {
-            const double v = x[i];
+            const double v = xs[i];
             fin &= isfinite(v);
             const uint32_t b = cbucket(order_key(v), hm, scale, nbtot);
             bk[k >> 1] |= b << ((k & 1) * 16);
@@ -632,23 +670,25 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
         cluster.sync();
         return;
     }
-    if (tid == 0) {
-        int over = 0;
-        uint32_t base = 0, total = 0;
-        for (int d = 0; d < CL; ++d) {
-            uint32_t col = 0, mine = 0;
+    if (wid == 0) {  // lane d: owner d's receive total and this CTA's offset in it
+        uint32_t col = 0, mine = 0;
+        if (lane < CL)
             for (int q = 0; q < CL; ++q) {
-                col += s_mat[q * CL + d];
-                if (q < r) mine += s_mat[q * CL + d];
+                const uint32_t v = s_mat[q * CL + lane];
+                col += v;
+                if (q < r) mine += v;
             }
-            s_off[d] = mine;
-            if (col > RCAP) over = 1;
-            if (d < r) base += col;
-            if (d == r) total = col;
+        if (lane < CL) s_off[lane] = mine;
+        const bool over = __any_sync(0xffffffffu, lane < CL && col > RCAP);
+        uint32_t below = lane < r ? col : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+        const uint32_t total = __shfl_sync(0xffffffffu, col, r);
+        if (lane == 0) {
+            s_total = total;
+            s_base = below;
+            s_over = over;
         }
-        s_total = total;
-        s_base = base;
-        s_over = over;
     }
     __syncthreads();
     if (s_over) {
@@ -663,16 +703,28 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     // ---- 3. scatter keys to the owners (one 8-byte DSMEM store per element).
     // The owner never needs the row: its outputs are written per receive slot
     // and the row finds them through route[row] = (owner, slot).
+    constexpr int SB = 8;  // slice reloads in flight per thread (L2 hits)
 #pragma unroll
-    for (int k = 0; k < EMAX; ++k) {
+    for (int h = 0; h < EMAX; h += SB) {
+      if (a + h * CT >= e) break;
+      double xv[SB];
+#pragma unroll
+      for (int k = 0; k < SB; ++k) {
+        const uint32_t i = a + (h + k) * CT + tid;
+        xv[k] = i < e ? x[i] : 0.0;
+      }
+#pragma unroll
+      for (int kk2 = 0; kk2 < SB; ++kk2) {
+        const int k = h + kk2;
         const uint32_t i = a + k * CT + tid;
         if (i < e) {
-            const unsigned long long kk = order_key(x[i]);
+            const unsigned long long kk = order_key(xv[kk2]);
             const uint32_t d = ((bk[k >> 1] >> ((k & 1) * 16)) & 0xffffu) >> lg_nbl;
             const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
             route[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = (d << 16) | slot;
             *cluster.map_shared_rank(recv_key + slot, d) = kk;
         }
+      }
     }
     cluster.sync();  // every receive buffer is complete; no DSMEM access after this point
     mark(3);
