@@ -397,10 +397,12 @@ inline ClusterPlan plan_for(uint64_t nmax, int cl) {
     const uint32_t slack = std::max<uint32_t>(256u, static_cast<uint32_t>(6.0 * std::sqrt(static_cast<double>(p.s))));
     p.rcap = (p.s + slack + 31u) & ~31u;
     uint32_t lg = 1;
-    while ((2u << lg) <= std::max<uint32_t>(2u, p.s / 2)) ++lg;  // NBL = largest power of two <= S/2 (>= 2)
+    while ((2u << lg) <= std::max<uint32_t>(2u, p.s)) ++lg;  // NBL = largest power of two <= S (>= 2)
     p.lg_nbl = lg;
-    // recv key 8 + row 4 + perm 2 per slot; NBL u16 counters/cursors + NBL+2 u16 starts
-    p.smem = static_cast<size_t>(p.rcap) * 14 + (static_cast<size_t>(1u << lg) * 2 + 4) * 2 + 64;
+    // per slot: key 8 + result 4 (aliased by the NBL u16 counters and the
+    // slot's u16 local bucket during the local sort; NBL <= S < RCAP) + perm 2;
+    // NBL+2 u16 bucket starts
+    p.smem = static_cast<size_t>(p.rcap) * 14 + (static_cast<size_t>(1u << lg) + 2) * 2 + 64;
     return p;
 }
 
@@ -411,7 +413,7 @@ inline ClusterPlan plan_cluster(uint64_t nmax) {
         if (forced && cl != forced) continue;
         ClusterPlan p = plan_for(nmax, cl);
         if (p.rcap <= static_cast<uint32_t>(QMAX * CT) && p.rcap < 32768 && p.smem <= kSmemLimit && p.s <= static_cast<uint32_t>(EMAX * CT) &&
-            (static_cast<uint64_t>(cl) << p.lg_nbl) <= 65536)
+            (static_cast<uint64_t>(cl) << p.lg_nbl) <= (1u << 20))
             return p;
     }
     return ClusterPlan{};
@@ -489,9 +491,10 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
 
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* recv_key = reinterpret_cast<unsigned long long*>(smem);
-    uint32_t* outw = reinterpret_cast<uint32_t*>(recv_key + RCAP);  // local bucket, then the slot's result
-    uint32_t* lhw = outw + RCAP;                            // NBL u16 counts -> cursors, two per word
-    uint16_t* lhs = reinterpret_cast<uint16_t*>(lhw + NBL / 2);  // NBL+1 u16 starts (+1 pad)
+    uint32_t* outw = reinterpret_cast<uint32_t*>(recv_key + RCAP);  // the slot's result (after the sort)
+    uint32_t* lhw = outw;                                   // during the sort: NBL u16 counts -> cursors
+    uint16_t* lbs = reinterpret_cast<uint16_t*>(lhw + NBL / 2);  // during the sort: local bucket per slot
+    uint16_t* lhs = reinterpret_cast<uint16_t*>(outw + RCAP);    // NBL+1 u16 starts (+1 pad)
     uint16_t* perm = lhs + NBL + 2;
 
     // the slice is staged into the (not yet used) receive buffer by one bulk
@@ -570,15 +573,22 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
             }
         }
     };
-    auto cluster_extremes = [&]() {
-        if (tid == 0) {
+    auto cluster_extremes = [&]() {  // lane q reads CTA q's extremes (parallel DSMEM loads)
+        if (wid == 0) {
             unsigned long long gmn = ~0ull, gmx = 0ull;
-            for (int q = 0; q < CL; ++q) {
-                gmn = min(gmn, *cluster.map_shared_rank(&s_rmin, q));
-                gmx = max(gmx, *cluster.map_shared_rank(&s_rmax, q));
+            if (lane < CL) {
+                gmn = *cluster.map_shared_rank(&s_rmin, lane);
+                gmx = *cluster.map_shared_rank(&s_rmax, lane);
             }
-            s_gmin = gmn;
-            s_gmax = gmx;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                gmn = min(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
+                gmx = max(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+            }
+            if (lane == 0) {
+                s_gmin = gmn;
+                s_gmax = gmx;
+            }
         }
         __syncthreads();
     };
@@ -627,9 +637,9 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
 
     // ---- 2. per-warp counts of what this CTA sends to each value-range owner;
     // each element's global bucket is kept (16 bits, two per register)
-    uint32_t bk[(EMAX + 1) / 2];
+    uint32_t bk[EMAX / 8];  // owner (4 bits) per element
 #pragma unroll
-    for (int k = 0; k < (EMAX + 1) / 2; ++k) bk[k] = 0u;
+    for (int k = 0; k < EMAX / 8; ++k) bk[k] = 0u;
     bool fin = true;
     wait_slice();  // the mbarrier was initialised before the first __syncthreads
 #pragma unroll
@@ -639,7 +649,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
             const double v = xs[i];
             fin &= isfinite(v);
             const uint32_t b = cbucket(order_key(v), hm, scale, nbtot);
-            bk[k >> 1] |= b << ((k & 1) * 16);
+            bk[k >> 3] |= (b >> lg_nbl) << ((k & 7) * 4);
             atomicAdd(&s_wc[wid][b >> lg_nbl], 1u);
         }
     }
@@ -656,10 +666,9 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     cluster.sync();
     mark(1);
     if (tid < CL * CL) s_mat[tid] = *cluster.map_shared_rank(&s_cnt[tid % CL], tid / CL);  // [src][dst]
-    if (tid == 0) {
-        int gb = 0;
-        for (int q = 0; q < CL; ++q) gb |= *cluster.map_shared_rank(&s_bad, q);
-        s_gbad = gb;
+    if (wid == 1) {
+        const int gb = __any_sync(0xffffffffu, lane < CL && *cluster.map_shared_rank(&s_bad, lane) != 0);
+        if (lane == 0) s_gbad = gb;
     }
     __syncthreads();
     if (s_gbad) {
@@ -719,7 +728,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
         const uint32_t i = a + k * CT + tid;
         if (i < e) {
             const unsigned long long kk = order_key(xv[kk2]);
-            const uint32_t d = ((bk[k >> 1] >> ((k & 1) * 16)) & 0xffffu) >> lg_nbl;
+            const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
             const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
             route[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = (d << 16) | slot;
             *cluster.map_shared_rank(recv_key + slot, d) = kk;
@@ -737,13 +746,13 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     __syncthreads();
     for (uint32_t j = tid; j < T; j += CT) {
         const uint32_t lb = cbucket(recv_key[j], hm, scale, nbtot) & lmask;
-        outw[j] = lb;
+        lbs[j] = static_cast<uint16_t>(lb);
         atomicAdd(lhw + (lb >> 1), 1u << ((lb & 1) * 16));
     }
     __syncthreads();
     block_scan_excl_u16(lhw, lhs, NBL, s_w);  // counts < 2^16: a bucket never exceeds RCAP < 65535
     for (uint32_t j = tid; j < T; j += CT) {
-        const uint32_t lb = outw[j], sh = (lb & 1) * 16;
+        const uint32_t lb = lbs[j], sh = (lb & 1) * 16;
         const uint32_t slot = (atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu;
         perm[slot] = static_cast<uint16_t>(j);
     }
@@ -756,10 +765,14 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     //   outw = (local r2 << 16) | local sorted position | run-start bit
     // walk the elements in bucket order: a warp's lanes mostly share buckets, so
     // the bucket-mate loads are shared-memory broadcasts
-    for (uint32_t qq = tid; qq < T; qq += CT) {
+    uint32_t keep[QMAX];  // results stay in registers while lbs (aliased by outw) is still read
+#pragma unroll
+    for (int k = 0; k < QMAX; ++k) {
+        const uint32_t qq = tid + k * CT;
+        if (qq >= T) break;
         const uint32_t j = perm[qq];
         const unsigned long long kv = recv_key[j];
-        const uint32_t lb = outw[j];
+        const uint32_t lb = lbs[j];
         const uint32_t s0 = lhs[lb], s1 = lhs[lb + 1];
         uint32_t less = 0, same = 0, before = 0;
 #pragma unroll 1
@@ -772,7 +785,14 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
             before += eqk && o < j;
         }
         const uint32_t llt = s0 + less;  // < T <= 16384, so local r2 = 2*llt + same + 1 <= 2T < 2^16
-        outw[j] = ((2u * llt + same + 1u) << 16) | (llt + before) | (before == 0 ? 0x8000u : 0u);
+        keep[k] = ((2u * llt + same + 1u) << 16) | (llt + before) | (before == 0 ? 0x8000u : 0u);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < QMAX; ++k) {
+        const uint32_t qq = tid + k * CT;
+        if (qq >= T) break;
+        outw[perm[qq]] = keep[k];
     }
     __syncthreads();
     const uint64_t reg = ((static_cast<uint64_t>(J.col) * K + J.seg) * CL + r) * RCAP;

@@ -275,10 +275,11 @@ __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const 
             if (lane == 0) s_tot = x;
         }
         cluster.sync();  // owner totals published
-        if (tid == 0) {  // owners above, in fixed order
-            double c = 0.0;
-            for (int q = r + 1; q < CL; ++q) c += *cluster.map_shared_rank(&s_tot, q);
-            s_carry = c;
+        if (wid == 0) {  // owners above (lane q reads owner q; fixed-order tree sum)
+            double c = (lane > r && lane < CL) ? *cluster.map_shared_rank(&s_tot, lane) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (lane == 0) s_carry = c;
         }
         __syncthreads();
         double carry = s_wo[wid] + s_carry;
