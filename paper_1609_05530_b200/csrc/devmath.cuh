@@ -116,7 +116,8 @@ struct GaussTheta {  // per-theta constants of copula.hpp:110-127
     }
 };
 
-__device__ __forceinline__ PointFull gauss_full(double x, double y, const GaussTheta& g) {
+// ex = exp(x^2/2), ey = exp(y^2/2) (rank-table entries when u is rank-derived)
+__device__ __forceinline__ PointFull gauss_full_e(double x, double y, double ex, double ey, const GaussTheta& g) {
     const double xy = x * y, ss = x * x + y * y;
     PointFull p;
     p.logc = g.half_log_a + (2.0 * g.t * xy - g.tt * ss) * (0.5 * g.ia);
@@ -124,9 +125,13 @@ __device__ __forceinline__ PointFull gauss_full(double x, double y, const GaussT
     p.hess = g.one_tt * g.ia2 + (g.c_hess_xy * xy - g.c_hess_ss * ss) * g.ia3;
     // cross_j = ((1+t^2) other - 2 t self) / (a^2 phi(self)); 1/phi(s) = sqrt(2pi) e^{s^2/2}
     const double k = 2.5066282746310002 * g.ia2;
-    p.cross1 = (g.one_tt * y - 2.0 * g.t * x) * (k * exp(0.5 * x * x));
-    p.cross2 = (g.one_tt * x - 2.0 * g.t * y) * (k * exp(0.5 * y * y));
+    p.cross1 = (g.one_tt * y - 2.0 * g.t * x) * (k * ex);
+    p.cross2 = (g.one_tt * x - 2.0 * g.t * y) * (k * ey);
     return p;
+}
+
+__device__ __forceinline__ PointFull gauss_full(double x, double y, const GaussTheta& g) {
+    return gauss_full_e(x, y, exp(0.5 * x * x), exp(0.5 * y * y), g);
 }
 
 // Sufficient-statistic form of the Gaussian pseudo-likelihood: with
@@ -343,19 +348,24 @@ __device__ __forceinline__ void gumbel_sh_f(float lx, float ly, const GumbelThet
 }
 
 // Full evaluation for the variance pass (copula.hpp:199-254), from
-// x = -ln u, y = -ln v and their logs.
-__device__ __forceinline__ PointFull gumbel_full_core(double u, double v, double x, double y, double lx, double ly,
-                                                      const GumbelTheta& g) {
+// lx = ln(-ln u), x = -ln u, ix = 1/x, iu = 1/u (and the same for v): the
+// rank-table entries when u is rank-derived. exp(a - m) of the larger
+// exponent is exactly 1, and exp(a - ln S) = exp(a - m) / S, so a point costs
+// four transcendentals.
+__device__ __forceinline__ PointFull gumbel_full_t(double lx, double ly, double x, double y, double ix, double iy,
+                                                   double iu, double iv, const GumbelTheta& g) {
     const double a = g.t * lx, b = g.t * ly;
-    const double m = fmax(a, b);
-    const double ea = exp(a - m), eb = exp(b - m);
-    const double sden = ea + eb;
+    const bool amax = a >= b;
+    const double m = amax ? a : b;
+    const double e = exp((amax ? b : a) - m);
+    const double ea = amax ? 1.0 : e, eb = amax ? e : 1.0;
+    const double sden = 1.0 + e;
     const double rs = 1.0 / sden;
     const double lnS = m + log(sden);
     const double w = exp(lnS * g.inv_t);
     const double r = (ea * lx + eb * ly) * rs;
     const double r2 = (ea * lx * lx + eb * ly * ly) * rs;
-    const double pa = exp(a - lnS) / x, pb = exp(b - lnS) / y;
+    const double pa = ea * rs * ix, pb = eb * rs * iy;
     const double rt = r2 - r * r;
     const double lw_t = r * g.inv_t - lnS * g.inv_t2;
     const double wt = w * lw_t;
@@ -372,27 +382,28 @@ __device__ __forceinline__ PointFull gumbel_full_core(double u, double v, double
     const double rg2 = rg * rg;
     {
         const double pt = pa * (lx - r);
-        const double cx = -wt * pa - w * pt + 1.0 / x - 2.0 * pa + (1.0 - 2.0 * g.t) * pt +
+        const double cx = -wt * pa - w * pt + ix - 2.0 * pa + (1.0 - 2.0 * g.t) * pt +
                           ((wt * pa + w * pt) * gg - w * pa * wt1) * rg2;
-        p.cross1 = -cx / u;
+        p.cross1 = -cx * iu;
     }
     {
         const double pt = pb * (ly - r);
-        const double cy = -wt * pb - w * pt + 1.0 / y - 2.0 * pb + (1.0 - 2.0 * g.t) * pt +
+        const double cy = -wt * pb - w * pt + iy - 2.0 * pb + (1.0 - 2.0 * g.t) * pt +
                           ((wt * pb + w * pt) * gg - w * pb * wt1) * rg2;
-        p.cross2 = -cy / v;
+        p.cross2 = -cy * iv;
     }
     return p;
 }
 
 __device__ __forceinline__ PointFull gumbel_full(double u, double v, const GumbelTheta& g) {
     const double x = -log(u), y = -log(v);
-    return gumbel_full_core(u, v, x, y, log(x), log(y), g);
+    return gumbel_full_t(log(x), log(y), x, y, 1.0 / x, 1.0 / y, 1.0 / u, 1.0 / v, g);
 }
 
 // from the hoisted (ln x, ln y) pair of the prepare pass
 __device__ __forceinline__ PointFull gumbel_full_l(double u, double v, double lx, double ly, const GumbelTheta& g) {
-    return gumbel_full_core(u, v, exp(lx), exp(ly), lx, ly, g);
+    const double x = exp(lx), y = exp(ly);
+    return gumbel_full_t(lx, ly, x, y, 1.0 / x, 1.0 / y, 1.0 / u, 1.0 / v, g);
 }
 
 // log c only (pseudo_loglik API), any family; u, v already clamped.

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
     if (with_fit ? status != kRunning : status != kConverged) return;
     const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);
     const uint32_t base = (tile - S.tile0) * FTILE;
-    const double* gt = gtab ? gtab + goff[m] : nullptr;
+    const double* gt = gtab ? gtab + 4 * goff[m] : nullptr;  // 4 doubles per rank entry
     const bool rt = R.routed && R.routed[m];
     double v[2] = {0.0, 0.0};
     constexpr int U = 4;  // points per thread in flight
@@ -225,8 +225,8 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
                     uu[j] = __dmul_rn(0.5 * static_cast<double>(r1), scale);
                     ww[j] = __dmul_rn(0.5 * static_cast<double>(r2), scale);
                     if (gt) {
-                        gx[j] = gt[r1];
-                        gy[j] = gt[r2];
+                        gx[j] = gt[4 * r1];
+                        gy[j] = gt[4 * r2];
                     }
                 }
             }
@@ -424,14 +424,27 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
     }
 }
 
-// The theta-independent per-point transform of u = (0.5*r2)/(n+1) for every
-// r2 in [2, 2n] of a block of n ranked rows — Phi^-1(u) (Gaussian scores) or
-// ln(-ln u) (Gumbel) — with the same arithmetic as the per-point path.
+// The theta-independent per-point transforms of u = (0.5*r2)/(n+1) for every
+// r2 in [2, 2n] of a block of n ranked rows, one 32-byte entry (one L2
+// sector) per r2, with the same arithmetic as the per-point path:
+//   Gaussian {x = Phi^-1(u), exp(x^2/2), 0, 0}
+//   Gumbel   {ln(-ln u), -ln u (as exp of the former), 1/(-ln u), 1/u}
 __global__ void k_rank_table(double* tab, uint32_t n, int fam) {
     const double scale = 1.0 / (static_cast<double>(n) + 1.0);
     for (uint32_t r2 = blockIdx.x * blockDim.x + threadIdx.x; r2 <= 2 * n; r2 += gridDim.x * blockDim.x) {
         const double u = clamp_unit(__dmul_rn(0.5 * static_cast<double>(r2), scale));
-        tab[r2] = r2 < 2 ? 0.0 : (fam == kGaussian ? dev_phi_inv(u) : log(-log(u)));
+        double4 t = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (r2 >= 2) {
+            if (fam == kGaussian) {
+                const double x = dev_phi_inv(u);
+                t = make_double4(x, exp(0.5 * x * x), 0.0, 0.0);
+            } else {
+                const double lx = log(-log(u)), x = exp(lx);
+                t = make_double4(lx, x, 1.0 / x, 1.0 / u);
+            }
+        }
+        reinterpret_cast<double2*>(tab)[2 * r2] = make_double2(t.x, t.y);
+        reinterpret_cast<double2*>(tab)[2 * r2 + 1] = make_double2(t.z, t.w);
     }
 }
 
@@ -624,7 +637,7 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
                 base[q] = tot;
                 tot += 2ull * sizes[q] + 1;
             }
-            auto* tab = c.ws.get_t<double>("fit.gtab", tot);
+            auto* tab = c.ws.get_t<double>("fit.gtab", 4 * tot);  // 4 doubles per entry
             std::vector<uint64_t> hoff(K);
             for (int m = 0; m < K; ++m)
                 hoff[m] = base[std::find(sizes.begin(), sizes.end(), segs[m].n) - sizes.begin()];
@@ -632,7 +645,8 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
             PCB_CUDA(cudaMemcpyAsync(d_off, hoff.data(), K * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
             for (size_t q = 0; q < sizes.size(); ++q) {
                 const uint32_t nn = sizes[q];
-                k_rank_table<<<std::min<uint32_t>(148u * 8u, (2 * nn + 256) / 256), 256, 0, s>>>(tab + base[q], nn, fam);
+                k_rank_table<<<std::min<uint32_t>(148u * 8u, (2 * nn + 256) / 256), 256, 0, s>>>(tab + 4 * base[q], nn,
+                                                                                                   fam);
                 c.count_launch();
             }
             gtab = tab;
@@ -696,8 +710,11 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
         v.rank = io.rank;
         v.u1 = io.u1;
         v.u2 = io.u2;
-        v.T64 = ((fam == kGaussian && !gtab) || (fam == kGumbel && !fp32T)) ? static_cast<const double2*>(T) : nullptr;
+        // Gaussian: the rank table (x, exp(x^2/2)) replaces T; Gumbel re-reads
+        // T (coalesced) rather than gathering 32-byte table entries at random
         v.gtab = fam == kGaussian ? gtab : nullptr;
+        v.T64 = (!v.gtab && (fam == kGaussian || (fam == kGumbel && !fp32T))) ? static_cast<const double2*>(T)
+                                                                               : nullptr;
         v.goff = goff;
         v.partials = part;
         v.tickets = tick;

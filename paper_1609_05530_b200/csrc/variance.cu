@@ -59,15 +59,23 @@ struct ThetaOf<kGumbel> {
     using type = GumbelTheta;
 };
 
-template <int FAM>
+// Where a point's theta-independent transforms come from
+enum { kFromU = 0, kFromT64 = 1, kFromTable = 2 };
+
+template <int FAM, int MODE>
 __device__ __forceinline__ PointFull eval_point(const typename ThetaOf<FAM>::type& th, double u, double w,
-                                                const double2& t64, bool has_t) {
+                                                const double2& t64, const double2 (&ta)[2], const double2 (&tb)[2]) {
     if constexpr (FAM == kGaussian) {
-        return gauss_full(has_t ? t64.x : dev_phi_inv(u), has_t ? t64.y : dev_phi_inv(w), th);
+        if constexpr (MODE == kFromTable) return gauss_full_e(ta[0].x, tb[0].x, ta[0].y, tb[0].y, th);
+        else if constexpr (MODE == kFromT64) return gauss_full(t64.x, t64.y, th);
+        else return gauss_full(dev_phi_inv(u), dev_phi_inv(w), th);
     } else if constexpr (FAM == kFrank) {
         return frank_full(u, w, th);
     } else {
-        return has_t ? gumbel_full_l(u, w, t64.x, t64.y, th) : gumbel_full(u, w, th);
+        if constexpr (MODE == kFromTable)
+            return gumbel_full_t(ta[0].x, tb[0].x, ta[0].y, tb[0].y, ta[1].x, tb[1].x, ta[1].y, tb[1].y, th);
+        else if constexpr (MODE == kFromT64) return gumbel_full_l(u, w, t64.x, t64.y, th);
+        else return gumbel_full(u, w, th);
     }
 }
 
@@ -82,7 +90,10 @@ __device__ __forceinline__ double with_flag(double x, bool f) {
 __device__ __forceinline__ bool flag_of(double x) { return (__double_as_longlong(x) & 1ll) != 0; }
 
 // ------------------------------------------------------------ pass 1
-template <int FAM>
+// MODE: where the theta-independent transforms come from (only that path is
+// compiled in). With the rank table a Gaussian point needs no transcendental
+// and a Gumbel point four.
+template <int FAM, int MODE>
 __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* segs, int nseg, RankRef R,
                                                  const double* __restrict__ u1, const double* __restrict__ u2,
                                                  const double2* __restrict__ T64, const double* __restrict__ gtab,
@@ -96,17 +107,17 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
     const typename ThetaOf<FAM>::type th(st[m].theta);
     const double scale = 1.0 / (static_cast<double>(S.n) + 1.0);
     const uint32_t base = (tile - S.tile0) * FTILE;
-    const double* gt = gtab ? gtab + goff[m] : nullptr;
-    const bool has_t = gt || T64;
+    const double2* gt = MODE == kFromTable ? reinterpret_cast<const double2*>(gtab + 4 * goff[m]) : nullptr;
     const bool rt = R.routed && R.routed[m];
     const uint64_t c1 = rt ? slot_index(R, nseg, 0, m, 0u) : 0, c2 = rt ? slot_index(R, nseg, 1, m, 0u) : 0;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
-    constexpr int U = 2;  // points per thread in flight
+    constexpr int U = (FAM == kGaussian && MODE == kFromTable) ? 4 : 2;  // points per thread in flight
     for (int k0 = 0; k0 < PPT; k0 += U) {
         unsigned long long p1[U], p2[U];  // packed ranks (by-row blocks)
         uint32_t w1[U], w2[U];            // route words (routed blocks)
         uint32_t q1[U], q2[U];            // r2
         double2 tt[U];
+        double2 ta[U][2], tb[U][2];  // rank-table entries of the two columns
         double uu[U], ww[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
@@ -124,7 +135,7 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
                     uu[j] = u1[row];
                     ww[j] = u2[row];
                 }
-                if (T64) tt[j] = T64[row];
+                if (MODE == kFromT64) tt[j] = T64[row];
             }
         }
 #pragma unroll
@@ -139,6 +150,19 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
                 q2[j] = R.r2s[c2 + (w2[j] >> 16) * R.rcap + (w2[j] & 0xffffu)];
             }
         }
+        if constexpr (MODE == kFromTable) {
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+                if (i >= S.n) continue;
+                ta[j][0] = gt[2 * q1[j]];
+                tb[j][0] = gt[2 * q2[j]];
+                if (FAM == kGumbel) {
+                    ta[j][1] = gt[2 * q1[j] + 1];
+                    tb[j][1] = gt[2 * q2[j] + 1];
+                }
+            }
+        }
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
@@ -148,8 +172,7 @@ __global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* seg
             double w = u1 ? ww[j] : __dmul_rn(0.5 * static_cast<double>(q2[j]), scale);
             u = clamp_unit(u);
             w = clamp_unit(w);
-            if (gt) tt[j] = make_double2(gt[q1[j]], gt[q2[j]]);
-            const PointFull p = eval_point<FAM>(th, u, w, tt[j], has_t);
+            const PointFull p = eval_point<FAM, MODE>(th, u, w, tt[j], ta[j], tb[j]);
             zb[row] = p.score;
             if (rt) {  // cross_j to (owner, slot) of the rank stage's route
                 xr[c1 + (w1[j] >> 16) * R.rcap + (w1[j] & 0xffffu)] = p.cross1;
@@ -486,8 +509,13 @@ __global__ void __launch_bounds__(FT) k_var_gather_g(BlockState* st, const Seg* 
 template <int FAM>
 void launch_var_point(Ctx& c, const VarIO& v, double* zb, double* Ag, double* xr) {
     const int K = static_cast<int>(v.off->size() - 1);
-    k_var_point<FAM><<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, v.rank->ref(), v.u1, v.u2, v.T64, v.gtab,
-                                                   v.goff, v.n_rows, zb, Ag, xr, v.partials, v.tickets);
+#define PCB_VAR_POINT(MODE)                                                                                   \
+    k_var_point<FAM, MODE><<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, v.rank->ref(), v.u1, v.u2, v.T64, v.gtab, \
+                                                         v.goff, v.n_rows, zb, Ag, xr, v.partials, v.tickets)
+    if (FAM != kFrank && v.gtab) PCB_VAR_POINT(kFromTable);
+    else if (FAM != kFrank && v.T64) PCB_VAR_POINT(kFromT64);
+    else PCB_VAR_POINT(kFromU);
+#undef PCB_VAR_POINT
     c.count_launch();
 }
 
