@@ -14,13 +14,14 @@
 //   block sums I, C_1, C_2, loglik. cross_j leaves along the route the rank
 //   stage's all-to-all took (owner CTA, receive slot): a warp's 32 consecutive
 //   rows land in a few short runs of slots, so the scatter is semi-coalesced.
-// Pass 2 (k_var_scan, one thread-block cluster per block, the rank stage's
-//   owners): each owner loads its received slots (coalesced), places them at
-//   their owner-local sorted positions in shared memory, suffix-scans with the
-//   higher owners' totals as carry (the only DSMEM traffic: CL doubles), and
-//   writes W_j back per slot (coalesced). Tie runs never straddle owners.
-// Pass 3 (k_var_final, grid of tiles): z = score + W_1 + W_2 per row through
-//   the route, sum z^2 -> M-hat -> sigma2.
+// Pass 2 (k_var_scan, one CTA per (column, block, owner) of the rank stage,
+//   independent of each other): load the owner's slots (coalesced), place
+//   them at their owner-local sorted positions in shared memory, suffix-scan
+//   locally, write the local suffix sum at each slot's tie-run start back per
+//   slot (coalesced) and the owner's total. Tie runs never straddle owners.
+//   k_var_carry turns the totals into each owner's carry (mass above it).
+// Pass 3 (k_var_final, grid of tiles): W_j = (local + carry - C_j)/n and
+//   z = score + W_1 + W_2 per row through the route, sum z^2 -> M-hat -> sigma2.
 // Blocks the rank stage did not route (global-path ranks, constant columns)
 // take the same steps through sorted-order arrays in global memory.
 // Deterministic: positions are unique, scans and sums run in fixed order.
@@ -208,19 +209,23 @@ __device__ __forceinline__ double finish_sigma2(BlockState& s, double zz, double
 }
 
 // ------------------------------------------------------------ pass 2 (routed)
-// Cluster of the block's CL owners; CTA r holds owner r's slots. Per column:
-// place, suffix-scan with carry from owners above, W per slot in place.
-// Thread t handles slots t + k*VT (k < JMAX; the rank plan keeps RCAP <=
-// JMAX*VT), so a slot's local position stays in registers from the place
-// step to the W step. The run-start flag rides in the LSB of the placed
-// cross value and becomes a bitmap in the scan's first pass.
+// One CTA per (column, block, owner) region, independent of the others: the
+// owner's slots are placed at their owner-local sorted positions in shared
+// memory, suffix-scanned locally, and L = local suffix sum at the slot's
+// tie-run start is written back per slot; the owner's total goes to `tot`.
+// The higher owners' mass (carry) is added in pass 3, so no CTA waits on
+// another. Thread t handles slots t + k*VT (k < JMAX; the rank plan keeps
+// RCAP <= JMAX*VT), so a slot's local position stays in registers from the
+// place step to the write-back. The run-start flag rides in the LSB of the
+// placed cross value and becomes a bitmap in the scan's first pass.
 constexpr int JMAX = 16;
 constexpr int JH = 4;  // loads in flight per thread in the place step
 
 __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const int* seg_list, int nseg,
-                                                   const Seg* segs, const uint16_t* __restrict__ posl,
-                                                   const uint32_t* __restrict__ ocnt, double* __restrict__ xr, int CL,
-                                                   uint32_t RCAP, unsigned long long* prof) {
+                                                   const uint16_t* __restrict__ posl,
+                                                   const uint32_t* __restrict__ ocnt, double* __restrict__ xr,
+                                                   double* __restrict__ tot, int CL, uint32_t RCAP,
+                                                   unsigned long long* prof) {
     long long t_prev = clock64();
     auto mark = [&](int k) {  // optional phase timing (PCB_VAR_PROFILE)
         if (prof && threadIdx.x == 0) {
@@ -229,125 +234,128 @@ __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const 
             t_prev = t;
         }
     };
-    cg::cluster_group cluster = cg::this_cluster();
-    const int r = static_cast<int>(cluster.block_rank());
-    const int m = seg_list[blockIdx.x / CL];
-    if (st[m].status != kConverged) return;  // uniform across the cluster, before any DSMEM access
-    const double inv_n = 1.0 / static_cast<double>(segs[m].n);
+    const int njobs = gridDim.x / (2 * CL);
+    const int col = blockIdx.x / (njobs * CL);
+    const int rem = blockIdx.x - col * njobs * CL;
+    const int m = seg_list[rem / CL];
+    const int r = rem % CL;
+    if (st[m].status != kConverged) return;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
     extern __shared__ __align__(16) unsigned char smem[];
     double* A = reinterpret_cast<double*>(smem);             // owner-local sorted positions
     uint32_t* bits = reinterpret_cast<uint32_t*>(A + RCAP);  // run-start bit per position
-    __shared__ double s_tot, s_carry;
     __shared__ double s_wt[VNW], s_wo[VNW];
 
-    for (int col = 0; col < 2; ++col) {
-        const double cj = col ? st[m].c2 : st[m].c1;
-        const uint64_t reg = ((static_cast<uint64_t>(col) * nseg + m) * CL + r) * RCAP;
-        const uint32_t T = ocnt[(static_cast<uint64_t>(col) * nseg + m) * CL + r];
-        double* X = xr + reg;
-        const uint16_t* P = posl + reg;
-        cluster.sync();  // the previous column is finished everywhere (s_tot, A, bits reusable)
-        mark(0);
-        // place: coalesced slot loads (JH in flight), random shared-memory stores
-        uint32_t pk[JMAX / 2];  // this thread's local positions, two per register
+    const uint64_t rid = (static_cast<uint64_t>(col) * nseg + m) * CL + r;
+    const uint64_t reg = rid * RCAP;
+    const uint32_t T = ocnt[rid];
+    double* X = xr + reg;
+    const uint16_t* P = posl + reg;
+    mark(0);
+    // place: coalesced slot loads (JH in flight), random shared-memory stores
+    uint32_t pk[JMAX / 2];  // this thread's local positions, two per register
 #pragma unroll
-        for (int h = 0; h < JMAX; h += JH) {
-            double x[JH];
-            uint32_t pv[JH];
+    for (int h = 0; h < JMAX; h += JH) {
+        double x[JH];
+        uint32_t pv[JH];
 #pragma unroll
-            for (int k = 0; k < JH; ++k) {
-                const uint32_t j = tid + (h + k) * VT;
-                if (j < T) {
-                    x[k] = X[j];
-                    pv[k] = P[j];
-                } else {
-                    pv[k] = 0xffffu;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < JH; ++k) {
-                if (pv[k] != 0xffffu) A[pv[k] & 0x7fffu] = with_flag(x[k], (pv[k] & 0x8000u) != 0);
-                if (k & 1) pk[(h + k) >> 1] = pv[k - 1] | (pv[k] << 16);
+        for (int k = 0; k < JH; ++k) {
+            const uint32_t j = tid + (h + k) * VT;
+            if (j < T) {
+                x[k] = X[j];
+                pv[k] = P[j];
+            } else {
+                pv[k] = 0xffffu;
             }
         }
-        __syncthreads();
-        mark(1);
-        // warp w scans the contiguous positions [w*WL, (w+1)*WL) (32-aligned)
-        const uint32_t WL = ((T + VNW - 1) / VNW + 31) & ~31u;
-        const uint32_t w0 = min(T, wid * WL), w1 = min(T, w0 + WL);
-        double wsum = 0.0;
-        for (uint32_t q = w0 + lane; q - lane < w1; q += 32) {
-            const double v = q < w1 ? A[q] : 0.0;
-            const unsigned fl = __ballot_sync(0xffffffffu, q < w1 && flag_of(v));
-            if (lane == 0) bits[q >> 5] = fl;
-            wsum += v;
-        }
-        wsum = warp_sum(wsum);
-        if (lane == 0) s_wt[wid] = wsum;
-        __syncthreads();
-        if (wid == 0) {  // exclusive suffix of the warp totals; owner total
-            double x = s_wt[lane];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_down_sync(0xffffffffu, x, o);
-                if (lane + o < 32) x += y;
-            }
-            s_wo[lane] = x - s_wt[lane];
-            if (lane == 0) s_tot = x;
+        for (int k = 0; k < JH; ++k) {
+            if (pv[k] != 0xffffu) A[pv[k] & 0x7fffu] = with_flag(x[k], (pv[k] & 0x8000u) != 0);
+            if (k & 1) pk[(h + k) >> 1] = pv[k - 1] | (pv[k] << 16);
         }
-        cluster.sync();  // owner totals published
-        if (wid == 0) {  // owners above (lane q reads owner q; fixed-order tree sum)
-            double c = (lane > r && lane < CL) ? *cluster.map_shared_rank(&s_tot, lane) : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-            if (lane == 0) s_carry = c;
-        }
-        __syncthreads();
-        double carry = s_wo[wid] + s_carry;
-        for (uint32_t t = (w1 - w0 + 31) / 32; t-- > 0;) {
-            const uint32_t q = w0 + t * 32 + lane;
-            double x = q < w1 ? A[q] : 0.0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_down_sync(0xffffffffu, x, o);
-                if (lane + o < 32) x += y;
-            }
-            if (q < w1) A[q] = carry + x;
-            carry += __shfl_sync(0xffffffffu, x, 0);
-        }
-        __syncthreads();
-        mark(2);
-        // W_j per slot: suffix sum at the start of the slot's tie run (owner-local)
-#pragma unroll
-        for (int k = 0; k < JMAX; ++k) {
-            const uint32_t j = tid + k * VT;
-            if (j >= T) break;
-            const uint32_t pv = (pk[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
-            uint32_t q = pv & 0x7fffu;
-            if (!(pv & 0x8000u)) {
-                uint32_t t = q - 1;  // position 0 of an owner always starts a run
-                for (;;) {
-                    const uint32_t w = bits[t >> 5] & (0xffffffffu >> (31 - (t & 31)));
-                    if (w) {
-                        q = (t & ~31u) + (31 - __clz(w));
-                        break;
-                    }
-                    t = (t & ~31u) - 1;
-                }
-            }
-            X[j] = (A[q] - cj) * inv_n;
-        }
-        mark(3);
     }
-    cluster.sync();  // peers' s_tot reads are done
+    __syncthreads();
+    mark(1);
+    // warp w scans the contiguous positions [w*WL, (w+1)*WL) (32-aligned)
+    const uint32_t WL = ((T + VNW - 1) / VNW + 31) & ~31u;
+    const uint32_t w0 = min(T, wid * WL), w1 = min(T, w0 + WL);
+    double wsum = 0.0;
+    for (uint32_t q = w0 + lane; q - lane < w1; q += 32) {
+        const double v = q < w1 ? A[q] : 0.0;
+        const unsigned fl = __ballot_sync(0xffffffffu, q < w1 && flag_of(v));
+        if (lane == 0) bits[q >> 5] = fl;
+        wsum += v;
+    }
+    wsum = warp_sum(wsum);
+    if (lane == 0) s_wt[wid] = wsum;
+    __syncthreads();
+    if (wid == 0) {  // exclusive suffix of the warp totals; owner total
+        double x = s_wt[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_down_sync(0xffffffffu, x, o);
+            if (lane + o < 32) x += y;
+        }
+        s_wo[lane] = x - s_wt[lane];
+        if (lane == 0) tot[rid] = x;
+    }
+    __syncthreads();
+    double carry = s_wo[wid];
+    for (uint32_t t = (w1 - w0 + 31) / 32; t-- > 0;) {
+        const uint32_t q = w0 + t * 32 + lane;
+        double x = q < w1 ? A[q] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_down_sync(0xffffffffu, x, o);
+            if (lane + o < 32) x += y;
+        }
+        if (q < w1) A[q] = carry + x;
+        carry += __shfl_sync(0xffffffffu, x, 0);
+    }
+    __syncthreads();
+    mark(2);
+    // L per slot: local suffix sum at the start of the slot's tie run
+#pragma unroll
+    for (int k = 0; k < JMAX; ++k) {
+        const uint32_t j = tid + k * VT;
+        if (j >= T) break;
+        const uint32_t pv = (pk[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
+        uint32_t q = pv & 0x7fffu;
+        if (!(pv & 0x8000u)) {
+            uint32_t t = q - 1;  // position 0 of an owner always starts a run
+            for (;;) {
+                const uint32_t w = bits[t >> 5] & (0xffffffffu >> (31 - (t & 31)));
+                if (w) {
+                    q = (t & ~31u) + (31 - __clz(w));
+                    break;
+                }
+                t = (t & ~31u) - 1;
+            }
+        }
+        X[j] = A[q];
+    }
+    mark(3);
+}
+
+// carry[col][m][d] = mass of the owners above d (fixed order)
+__global__ void k_var_carry(const int* seg_list, int njobs, int nseg, int CL, const double* tot, double* carry) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= 2 * njobs) return;
+    const int col = q / njobs, m = seg_list[q % njobs];
+    const uint64_t b = (static_cast<uint64_t>(col) * nseg + m) * CL;
+    double c = 0.0;
+    for (int d = CL - 1; d >= 0; --d) {
+        carry[b + d] = c;
+        c += tot[b + d];
+    }
 }
 
 // z = score + W_1 + W_2 per row (through the route), sum z^2 -> sigma2
 __global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* segs, int nseg, RankRef R,
                                                  uint64_t n_rows, const double* __restrict__ zb,
-                                                 const double* __restrict__ xr, double* partials, unsigned* tickets) {
+                                                 const double* __restrict__ xr, const double* __restrict__ carry,
+                                                 double* partials, unsigned* tickets) {
     const uint32_t tile = blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
@@ -356,6 +364,10 @@ __global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* seg
     const uint32_t* route = R.route;
     const double* x1 = xr + slot_index(R, nseg, 0, m, 0u);
     const double* x2 = xr + slot_index(R, nseg, 1, m, 0u);
+    const double* k1 = carry + static_cast<uint64_t>(m) * R.cl;
+    const double* k2 = carry + (static_cast<uint64_t>(nseg) + m) * R.cl;
+    const double cj1 = st[m].c1, cj2 = st[m].c2;
+    const double inv_n = 1.0 / static_cast<double>(S.n);
     const uint32_t base = (tile - S.tile0) * FTILE;
     double v[1] = {0.0};
     constexpr int U = 4;
@@ -377,8 +389,8 @@ __global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* seg
         for (int j = 0; j < U; ++j) {
             const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
             if (i < S.n) {
-                w1[j] = x1[(r1[j] >> 16) * RCAP + (r1[j] & 0xffffu)];
-                w2[j] = x2[(r2[j] >> 16) * RCAP + (r2[j] & 0xffffu)];
+                w1[j] = x1[(r1[j] >> 16) * RCAP + (r1[j] & 0xffffu)] + k1[r1[j] >> 16];
+                w2[j] = x2[(r2[j] >> 16) * RCAP + (r2[j] & 0xffffu)] + k2[r2[j] >> 16];
             }
         }
 #pragma unroll
@@ -386,8 +398,8 @@ __global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* seg
             const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
             if (i < S.n) {
                 double z = zz[j];
-                z += w1[j];
-                z += w2[j];
+                z += (w1[j] - cj1) * inv_n;
+                z += (w2[j] - cj2) * inv_n;
                 v[0] += z * z;
             }
         }
@@ -519,41 +531,26 @@ void launch_var_point(Ctx& c, const VarIO& v, double* zb, double* Ag, double* xr
     c.count_launch();
 }
 
-void launch_var_scan(Ctx& c, const VarIO& v, const int* seg_list, int njobs, double* xr) {
+void launch_var_scan(Ctx& c, const VarIO& v, const int* seg_list, int njobs, double* xr, double* tot) {
     const RankOut& R = *v.rank;
     const int K = static_cast<int>(v.off->size() - 1);
     const size_t smem = static_cast<size_t>(R.rcap) * 8 + (R.rcap / 32 + 1) * 4;
     PCB_CUDA(cudaFuncSetAttribute(k_var_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    if (R.cl > 8) PCB_CUDA(cudaFuncSetAttribute(k_var_scan, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(njobs) * static_cast<unsigned>(R.cl));
-    cfg.blockDim = dim3(VT);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = static_cast<unsigned>(R.cl);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
     unsigned long long* prof = nullptr;
     const char* pe = std::getenv("PCB_VAR_PROFILE");
     if (pe && pe[0] == '1') {
         prof = c.ws.get_t<unsigned long long>("var.prof", 8);
         PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
     }
-    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_var_scan, static_cast<const BlockState*>(v.st), seg_list, K,
-                                static_cast<const Seg*>(v.segs), static_cast<const uint16_t*>(R.posl),
-                                static_cast<const uint32_t*>(R.ocnt), xr, R.cl, R.rcap, prof));
+    const unsigned grid = 2u * static_cast<unsigned>(njobs) * static_cast<unsigned>(R.cl);
+    k_var_scan<<<grid, VT, smem, c.stream>>>(v.st, seg_list, K, R.posl, R.ocnt, xr, tot, R.cl, R.rcap, prof);
     c.count_launch();
     if (prof) {
         unsigned long long h[8];
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
         PCB_CUDA(cudaStreamSynchronize(c.stream));
-        const double ctas = static_cast<double>(njobs) * R.cl;
-        std::fprintf(stderr, "[var profile] CL=%d rcap=%u cycles/CTA (both columns): sync %.0f  place %.0f  scan %.0f  W %.0f\n",
-                     R.cl, R.rcap, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas);
+        std::fprintf(stderr, "[var profile] CL=%d rcap=%u cycles/CTA (one column): start %.0f  place %.0f  scan %.0f  write %.0f\n",
+                     R.cl, R.rcap, h[0] / double(grid), h[1] / double(grid), h[2] / double(grid), h[3] / double(grid));
     }
 }
 
@@ -593,10 +590,14 @@ void run_variance(Ctx& c, const VarIO& v) {
             if (R.routed[m]) jobs.push_back(m);
         int* d_jobs = c.ws.get_t<int>("var.jobs", K);
         PCB_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
-        launch_var_scan(c, v, d_jobs, static_cast<int>(jobs.size()), xr);
-        k_var_final<<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, R.ref(), v.n_rows, zb, xr, v.partials,
+        const int nj = static_cast<int>(jobs.size());
+        auto* tot = c.ws.get_t<double>("var.tot", 2 * static_cast<size_t>(K) * R.cl);
+        auto* carry = c.ws.get_t<double>("var.carry", 2 * static_cast<size_t>(K) * R.cl);
+        launch_var_scan(c, v, d_jobs, nj, xr, tot);
+        k_var_carry<<<(2 * nj + 127) / 128, 128, 0, c.stream>>>(d_jobs, nj, K, R.cl, tot, carry);
+        k_var_final<<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, R.ref(), v.n_rows, zb, xr, carry, v.partials,
                                                   v.tickets);
-        c.count_launch();
+        c.count_launch(2);
     }
     if (nrouted < K) {
         std::vector<uint8_t> use(K);
