@@ -39,6 +39,7 @@ K_SUBSETS = 8000
 BASE_SEED = 0x160905530
 METRIC = "copula fit throughput (points/sec, fp64) at n=1e9, 1/2/4/8 B200, % roofline"
 # SURVEY.md §8(d) frozen algorithmic FP64 instructions per point per theta candidate (F_fit)
+PIPE_ROOF_PTS = {"gaussian": 6.8e10, "frank": 1.9e10, "gumbel": 1.4e10}  # SURVEY.md §8(d), per GPU
 F_FIT = {"gaussian": 9, "frank": 175, "gumbel": 210}
 F_VAR = {"gaussian": 24, "frank": 260, "gumbel": 350}  # per point at theta-hat (variance pass)
 B_PASS = 16  # bytes per point per likelihood pass (fp64 pair)
@@ -340,6 +341,12 @@ def run_ours(args):
                 "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/r01_ncu_v5.md, per point x points)",
                 "algorithmic_bytes_per_launch": per_kernel[dom][2] / max(per_kernel[dom][1], 1),
                 "per_kernel": table}
+        # SURVEY.md §8(d) pipeline roofline per GPU (B_pipe = 96 B/pt against HBM; F_pipe with the
+        # oracle's mean Newton passes against FP64): the step's floor for the C5 mix
+        floor_ms = sum(n / PIPE_ROOF_PTS[name] * 1e3 for name, _, _ in FAMILIES) / world
+        roof["pipeline"] = {"floor_ms_per_step": floor_ms, "frac": floor_ms / ms,
+                            "pts_per_s_per_gpu": PIPE_ROOF_PTS,
+                            "source": "SURVEY.md §8(d): Gaussian HBM 96 B/pt; Frank/Gumbel FP64 F_pipe (P=4/4.2)"}
     # ------------------------------------------------------------ e2e
     e2e = None
     if not args.no_e2e:
