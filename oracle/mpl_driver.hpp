@@ -332,20 +332,26 @@ struct Driver {
 
 // theta_c = sum w theta / sum w, w = 1/sigma2 over the
 // converged blocks, in block order. Returns the number of blocks used.
+// Eq. (15) anchored at the first used block's estimate a:
+//   theta_c = a + sum w (theta - a) / sum w  (== sum w theta / sum w),
+// which is exact in the SPEC's degenerate cases (M = 1 returns the full-data
+// fit bit for bit; constant estimates return the constant,
+// SPEC.md:290) where the plain ratio can be off by an ulp.
 inline size_t combine_records(const FitRecord* r, size_t k, double* theta_c, double* weights) {
-    double sw = 0.0, swt = 0.0;
+    double sw = 0.0, swd = 0.0, anchor = 0.0;
     size_t used = 0;
     for (size_t m = 0; m < k; ++m) {
         const bool ok = r[m].converged && r[m].sigma2 > 0.0 && std::isfinite(r[m].sigma2);
         const double w = ok ? 1.0 / r[m].sigma2 : 0.0;
         if (weights) weights[m] = w;
         if (!ok) continue;
+        if (used == 0) anchor = r[m].theta_hat;
         sw += w;
-        swt += w * r[m].theta_hat;
+        swd += w * (r[m].theta_hat - anchor);
         ++used;
     }
     if (used == 0) throw std::runtime_error("combine: no converged blocks");
-    *theta_c = swt / sw;
+    *theta_c = anchor + swd / sw;
     return used;
 }
 

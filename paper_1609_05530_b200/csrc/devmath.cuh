@@ -205,15 +205,17 @@ struct FrankThetaF {
 __device__ __forceinline__ void frank_sh_f(float u, float v, const FrankThetaF& f, float& s, float& h) {
     const float t = f.t;
     const float lo = fminf(u, v), hi = fmaxf(u, v);
-    const float ema = expm1f(-t * (1.0f - lo));
-    const float e2 = expf(-t * (hi - lo));
+    // warm-up accuracy suffices (the fp64 passes decide convergence): fast
+    // exponentials except where expm1 of a small argument needs the full one
+    const float ema = __expf(-t * (1.0f - lo)) - 1.0f;  // 1 - lo >= 1/2 after the radial reflection
+    const float e2 = __expf(-t * (hi - lo));
     const float emb = expm1f(-t * lo);
     const float e1 = 1.0f + ema, e3 = 1.0f + emb;
     const float b = ema + e2 * emb;
     const float sum = lo + hi;
     const float bp = lo - e1 + e2 * (hi - sum * e3);
     const float bpp = e1 - lo * lo + e2 * (sum * sum * e3 - hi * hi);
-    const float rb = 1.0f / b;
+    const float rb = __frcp_rn(b);
     const float q = bp * rb;
     s = f.inv_t - f.g - sum - 2.0f * q;
     h = f.hconst - 2.0f * (bpp * rb - q * q);
@@ -326,11 +328,11 @@ __device__ __forceinline__ void gumbel_sh_f(float lx, float ly, const GumbelThet
     const bool amax = a >= b;
     const float m = amax ? a : b;
     const float lmax = amax ? lx : ly, lmin = amax ? ly : lx;
-    const float e = expf((amax ? b : a) - m);
+    const float e = __expf((amax ? b : a) - m);
     const float sden = 1.0f + e;
-    const float rs = 1.0f / sden;
-    const float lnS = m + log1pf(e);
-    const float w = expf(lnS * g.inv_t);
+    const float rs = __frcp_rn(sden);
+    const float lnS = m + __logf(sden);  // warm-up accuracy (absolute error ~1e-7)
+    const float w = __expf(lnS * g.inv_t);
     const float r = (lmax + e * lmin) * rs;
     const float r2 = (lmax * lmax + e * lmin * lmin) * rs;
     const float d = lmax - lmin;  // r2 - r^2 = e d^2 / (1+e)^2, free of cancellation
@@ -341,7 +343,7 @@ __device__ __forceinline__ void gumbel_sh_f(float lx, float ly, const GumbelThet
     const float lw_tt = rt * g.inv_t - 2.0f * r * g.inv_t2 + 2.0f * lnS * g.inv_t3;
     const float wtt = w * (lw_t * lw_t + lw_tt);
     const float gg = w + g.t - 1.0f;
-    const float rg = 1.0f / gg;
+    const float rg = __frcp_rn(gg);
     const float wt1 = wt + 1.0f;
     s = -wt + lx + ly - lnS * g.inv_t2 + g.c1t * r + wt1 * rg;
     h = -wtt - 2.0f * r * g.inv_t2 + 2.0f * lnS * g.inv_t3 + g.c1t * rt + (wtt * gg - wt1 * wt1) * rg * rg;

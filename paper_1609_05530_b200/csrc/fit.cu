@@ -369,7 +369,8 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
                 }
             }
         }
-    } else {  // fp32 per-point arithmetic, fp64 accumulation
+    } else {  // fp32 per-point arithmetic: per-thread fp32 partial sums (PPT points), fp64 beyond
+        float fs = 0.0f, fh = 0.0f;
         if (FAM == kFrank) {
             const FrankThetaF f(theta);
 #pragma unroll 4
@@ -396,8 +397,8 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
                     }
                     float s, h;
                     frank_sh_f(uv, vv, f, s, h);
-                    v[0] += static_cast<double>(f.neg ? -s : s);
-                    v[1] += static_cast<double>(h);
+                    fs += f.neg ? -s : s;
+                    fh += h;
                 }
             }
         } else {
@@ -409,11 +410,13 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
                     const TI p = Tb[i];
                     float s, h;
                     gumbel_sh_f(p.x, p.y, g, s, h);
-                    v[0] += static_cast<double>(s);
-                    v[1] += static_cast<double>(h);
+                    fs += s;
+                    fh += h;
                 }
             }
         }
+        v[0] = fs;
+        v[1] = fh;
     }
     __shared__ double sh[(FT / 32) * 2];
     if (!tile_reduce<2>(v, sh, partials, tickets, S, m, tile)) return;

@@ -18,7 +18,21 @@ struct RecordIn {  // == pcb_fit_result
 // finite positive variance; theta_c = sum w theta / sum w. One CTA, fixed
 // strided assignment + fixed tree => bitwise identical for any split of the
 // blocks across GPUs (the gathered record array is the same bytes).
+// Eq. (15) anchored at the first used block (exact for M = 1 and constant
+// estimates); fixed-order reduction.
 __global__ void __launch_bounds__(1024) k_combine(const RecordIn* r, uint64_t n, double* weights, double* out) {
+    __shared__ unsigned long long s_first;
+    if (threadIdx.x == 0) s_first = ~0ull;
+    __syncthreads();
+    for (uint64_t m = threadIdx.x; m < n; m += blockDim.x) {
+        const RecordIn x = r[m];
+        if (x.converged && x.sigma2 > 0.0 && isfinite(x.sigma2)) {
+            atomicMin(&s_first, static_cast<unsigned long long>(m));
+            break;
+        }
+    }
+    __syncthreads();
+    const double anchor = s_first < n ? r[s_first].theta_hat : 0.0;
     double v[3] = {0.0, 0.0, 0.0};
     for (uint64_t m = threadIdx.x; m < n; m += blockDim.x) {
         const RecordIn x = r[m];
@@ -27,16 +41,16 @@ __global__ void __launch_bounds__(1024) k_combine(const RecordIn* r, uint64_t n,
         if (weights) weights[m] = w;
         if (ok) {
             v[0] += w;
-            v[1] += w * x.theta_hat;
+            v[1] += w * (x.theta_hat - anchor);
             v[2] += 1.0;
         }
     }
     __shared__ double sh[32 * 3];
     block_sum<3>(v, sh);
     if (threadIdx.x == 0) {
-        out[0] = v[2] > 0.0 ? v[1] / v[0] : NAN;  // theta_combined
-        out[1] = v[0];                            // total weight
-        out[2] = v[2];                            // blocks used
+        out[0] = v[2] > 0.0 ? anchor + v[1] / v[0] : NAN;  // theta_combined
+        out[1] = v[0];                                     // total weight
+        out[2] = v[2];                                     // blocks used
     }
 }
 

@@ -239,6 +239,17 @@ def test_strided_scheme(ctx, orc):
     check_records(res.per_block, recs, TOL64)
 
 
+def test_combine_spec_examples_on_device(ctx):  # SPEC.md:290-292, exact where the SPEC is exact
+    from paper_1609_05530_b200.parcop import FitResult
+    mk = lambda t, s: FitResult(t, s, 100, 0.0, 3, True)  # noqa: E731
+    assert pcb.combine([mk(0.3, 1.0), mk(0.3, 2.0), mk(0.3, 9.0)], ctx=ctx).theta_combined == 0.3
+    assert pcb.combine([mk(1.99112997922569, 2.0584161e-4)], ctx=ctx).theta_combined == 1.99112997922569
+    assert pcb.combine([mk(0.2, 1.0), mk(0.4, 4.0)], ctx=ctx).theta_combined == pytest.approx(0.24, rel=1e-15)
+    bad = FitResult(9.0, 1.0, 100, 0.0, 50, False)
+    r = pcb.combine([bad, mk(0.2, 2.0), mk(0.4, 2.0)], ctx=ctx)
+    assert r.blocks_used == 2 and r.theta_combined == pytest.approx(0.3, rel=1e-15)
+
+
 def test_m1_equals_full_fit(ctx):
     X = pcb.sample_matrix(2, 2.0, 20000, 1, ctx=ctx)
     res = pcb.fit_parallel(2, X, 1, ctx=ctx)

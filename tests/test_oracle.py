@@ -65,7 +65,8 @@ def test_spec_rank_examples(orc):
 def test_spec_combine_examples(orc):
     from oracle.oracle import FitRecord
     mk = lambda t, s: FitRecord(t, s, 0.0, 100, 3, 1, 0, 0)  # noqa: E731
-    assert orc.combine([mk(0.3, 1.0), mk(0.3, 2.0), mk(0.3, 9.0)])[0] == pytest.approx(0.3, abs=1e-16)
+    assert orc.combine([mk(0.3, 1.0), mk(0.3, 2.0), mk(0.3, 9.0)])[0] == 0.3  # exact (anchored Eq. 15)
+    assert orc.combine([mk(1.99112997922569, 2.0584161e-4)])[0] == 1.99112997922569  # M = 1
     assert orc.combine([mk(0.2, 2.0), mk(0.4, 2.0)])[0] == pytest.approx(0.3, rel=1e-15)
     assert orc.combine([mk(0.2, 1.0), mk(0.4, 4.0)])[0] == pytest.approx(0.24, rel=1e-15)
     bad = FitRecord(0.9, 1.0, 0.0, 100, 3, 0, 1, 0)
