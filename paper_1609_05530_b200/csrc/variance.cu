@@ -94,8 +94,25 @@ __device__ __forceinline__ bool flag_of(double x) { return (__double_as_longlong
 // MODE: where the theta-independent transforms come from (only that path is
 // compiled in). With the rank table a Gaussian point needs no transcendental
 // and a Gumbel point four.
+// resident CTAs per SM the register budget is sized for (0 = compiler's
+// choice). Measured at C5: Gumbel 3 (80 regs, -3 ms); forcing Gaussian or
+// Frank below the compiler's allocation spills and loses.
+#ifndef PCB_VOCC_G
+#define PCB_VOCC_G 0
+#endif
+#ifndef PCB_VOCC_F
+#define PCB_VOCC_F 0
+#endif
+#ifndef PCB_VOCC_U
+#define PCB_VOCC_U 3
+#endif
+template <int FAM>
+struct VarOcc {
+    static constexpr int value = FAM == kGaussian ? PCB_VOCC_G : (FAM == kFrank ? PCB_VOCC_F : PCB_VOCC_U);
+};
+
 template <int FAM, int MODE>
-__global__ void __launch_bounds__(FT) k_var_point(BlockState* st, const Seg* segs, int nseg, RankRef R,
+__global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState* st, const Seg* segs, int nseg, RankRef R,
                                                  const double* __restrict__ u1, const double* __restrict__ u2,
                                                  const double2* __restrict__ T64, const double* __restrict__ gtab,
                                                  const uint64_t* goff, uint64_t n_rows, double* __restrict__ zb,
