@@ -231,14 +231,17 @@ __device__ __forceinline__ double finish_sigma2(BlockState& s, double zz, double
 // memory, suffix-scanned locally, and L = local suffix sum at the slot's
 // tie-run start is written back per slot; the owner's total goes to `tot`.
 // The higher owners' mass (carry) is added in pass 3, so no CTA waits on
-// another. Thread t handles slots t + k*VT (k < JMAX; the rank plan keeps
-// RCAP <= JMAX*VT), so a slot's local position stays in registers from the
-// place step to the write-back. The run-start flag rides in the LSB of the
-// placed cross value and becomes a bitmap in the scan's first pass.
-constexpr int JMAX = 16;
-constexpr int JH = 4;  // loads in flight per thread in the place step
+// another.
+//   place: thread t loads slots t + k*ST (all its loads in flight; RCAP <=
+//          SJ*ST), stores each at its position, sets run-start bits
+//   scan:  thread t owns PT (odd: few bank conflicts) consecutive positions:
+//          thread sum -> block suffix of thread sums -> thread-serial suffix
+//   write: per slot, the suffix sum at its run start (bitmap search, local)
+constexpr int ST = 512;  // threads per scan CTA
+constexpr int SJ = 32;   // slots per thread (RCAP <= 16384)
+constexpr int SW = ST / 32;
 
-__global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const int* seg_list, int nseg,
+__global__ void __launch_bounds__(ST, 1) k_var_scan(const BlockState* st, const int* seg_list, int nseg,
                                                    const uint16_t* __restrict__ posl,
                                                    const uint32_t* __restrict__ ocnt, double* __restrict__ xr,
                                                    double* __restrict__ tot, int CL, uint32_t RCAP,
@@ -262,80 +265,80 @@ __global__ void __launch_bounds__(VT, 1) k_var_scan(const BlockState* st, const 
     extern __shared__ __align__(16) unsigned char smem[];
     double* A = reinterpret_cast<double*>(smem);             // owner-local sorted positions
     uint32_t* bits = reinterpret_cast<uint32_t*>(A + RCAP);  // run-start bit per position
-    __shared__ double s_wt[VNW], s_wo[VNW];
+    __shared__ double s_ws[SW], s_wo[SW];
 
     const uint64_t rid = (static_cast<uint64_t>(col) * nseg + m) * CL + r;
     const uint64_t reg = rid * RCAP;
     const uint32_t T = ocnt[rid];
     double* X = xr + reg;
     const uint16_t* P = posl + reg;
+    for (uint32_t q = tid; q <= T / 32; q += ST) bits[q] = 0u;
+    __syncthreads();
     mark(0);
-    // place: coalesced slot loads (JH in flight), random shared-memory stores
-    uint32_t pk[JMAX / 2];  // this thread's local positions, two per register
+    uint32_t pk[SJ / 2];  // this thread's local positions (| run-start bit), two per register
 #pragma unroll
-    for (int h = 0; h < JMAX; h += JH) {
-        double x[JH];
-        uint32_t pv[JH];
+    for (int h = 0; h < SJ; h += 16) {
+        if (tid + h * ST >= T) {
 #pragma unroll
-        for (int k = 0; k < JH; ++k) {
-            const uint32_t j = tid + (h + k) * VT;
-            if (j < T) {
-                x[k] = X[j];
-                pv[k] = P[j];
-            } else {
-                pv[k] = 0xffffu;
-            }
+            for (int k = 0; k < 8; ++k) pk[(h >> 1) + k] = 0xffffffffu;
+            continue;
+        }
+        double x[16];
+        uint32_t pv[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t j = tid + (h + k) * ST;
+            pv[k] = j < T ? P[j] : 0xffffu;
+            x[k] = j < T ? X[j] : 0.0;
         }
 #pragma unroll
-        for (int k = 0; k < JH; ++k) {
-            if (pv[k] != 0xffffu) A[pv[k] & 0x7fffu] = with_flag(x[k], (pv[k] & 0x8000u) != 0);
+        for (int k = 0; k < 16; ++k) {
+            if (pv[k] != 0xffffu) {
+                const uint32_t p = pv[k] & 0x7fffu;
+                A[p] = x[k];
+                if (pv[k] & 0x8000u) atomicOr(bits + (p >> 5), 1u << (p & 31));
+            }
             if (k & 1) pk[(h + k) >> 1] = pv[k - 1] | (pv[k] << 16);
         }
     }
     __syncthreads();
     mark(1);
-    // warp w scans the contiguous positions [w*WL, (w+1)*WL) (32-aligned)
-    const uint32_t WL = ((T + VNW - 1) / VNW + 31) & ~31u;
-    const uint32_t w0 = min(T, wid * WL), w1 = min(T, w0 + WL);
-    double wsum = 0.0;
-    for (uint32_t q = w0 + lane; q - lane < w1; q += 32) {
-        const double v = q < w1 ? A[q] : 0.0;
-        const unsigned fl = __ballot_sync(0xffffffffu, q < w1 && flag_of(v));
-        if (lane == 0) bits[q >> 5] = fl;
-        wsum += v;
+    // thread-contiguous suffix scan
+    const uint32_t PT = ((T + ST - 1) / ST) | 1u;
+    const uint32_t p0 = min(T, tid * PT), p1 = min(T, p0 + PT);
+    double ts = 0.0;
+    for (uint32_t q = p0; q < p1; ++q) ts += A[q];
+    double x = ts;  // inclusive suffix over the warp's threads (lanes above)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_down_sync(0xffffffffu, x, o);
+        if (lane + o < 32) x += y;
     }
-    wsum = warp_sum(wsum);
-    if (lane == 0) s_wt[wid] = wsum;
+    if (lane == 0) s_ws[wid] = x;
     __syncthreads();
     if (wid == 0) {  // exclusive suffix of the warp totals; owner total
-        double x = s_wt[lane];
+        double w = lane < SW ? s_ws[lane] : 0.0;
+        const double w0 = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_down_sync(0xffffffffu, x, o);
-            if (lane + o < 32) x += y;
+            const double y = __shfl_down_sync(0xffffffffu, w, o);
+            if (lane + o < 32) w += y;
         }
-        s_wo[lane] = x - s_wt[lane];
-        if (lane == 0) tot[rid] = x;
+        if (lane < SW) s_wo[lane] = w - w0;
+        if (lane == 0) tot[rid] = w;
     }
     __syncthreads();
-    double carry = s_wo[wid];
-    for (uint32_t t = (w1 - w0 + 31) / 32; t-- > 0;) {
-        const uint32_t q = w0 + t * 32 + lane;
-        double x = q < w1 ? A[q] : 0.0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_down_sync(0xffffffffu, x, o);
-            if (lane + o < 32) x += y;
-        }
-        if (q < w1) A[q] = carry + x;
-        carry += __shfl_sync(0xffffffffu, x, 0);
+    double acc = s_wo[wid] + (x - ts);  // mass above this thread's positions
+    for (uint32_t q = p1; q-- > p0;) {
+        acc += A[q];
+        A[q] = acc;
     }
     __syncthreads();
     mark(2);
     // L per slot: local suffix sum at the start of the slot's tie run
 #pragma unroll
-    for (int k = 0; k < JMAX; ++k) {
-        const uint32_t j = tid + k * VT;
+    for (int k = 0; k < SJ; ++k) {
+        const uint32_t j = tid + k * ST;
         if (j >= T) break;
         const uint32_t pv = (pk[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
         uint32_t q = pv & 0x7fffu;
@@ -560,7 +563,7 @@ void launch_var_scan(Ctx& c, const VarIO& v, const int* seg_list, int njobs, dou
         PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
     }
     const unsigned grid = 2u * static_cast<unsigned>(njobs) * static_cast<unsigned>(R.cl);
-    k_var_scan<<<grid, VT, smem, c.stream>>>(v.st, seg_list, K, R.posl, R.ocnt, xr, tot, R.cl, R.rcap, prof);
+    k_var_scan<<<grid, ST, smem, c.stream>>>(v.st, seg_list, K, R.posl, R.ocnt, xr, tot, R.cl, R.rcap, prof);
     c.count_launch();
     if (prof) {
         unsigned long long h[8];
