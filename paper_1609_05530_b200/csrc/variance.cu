@@ -259,7 +259,6 @@ __global__ void __launch_bounds__(ST, 1) k_var_scan(const BlockState* st, const 
     const int rem = blockIdx.x - col * njobs * CL;
     const int m = seg_list[rem / CL];
     const int r = rem % CL;
-    if (st[m].status != kConverged) return;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
     extern __shared__ __align__(16) unsigned char smem[];
@@ -269,9 +268,22 @@ __global__ void __launch_bounds__(ST, 1) k_var_scan(const BlockState* st, const 
 
     const uint64_t rid = (static_cast<uint64_t>(col) * nseg + m) * CL + r;
     const uint64_t reg = rid * RCAP;
-    const uint32_t T = ocnt[rid];
     double* X = xr + reg;
     const uint16_t* P = posl + reg;
+    // the first loads go out before the block's status and count arrive (the
+    // region is RCAP slots long, so reading past the count is in bounds)
+    double x0[16];
+    uint32_t pv0[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t j = tid + k * ST;
+        if (j < RCAP) {
+            pv0[k] = P[j];
+            x0[k] = X[j];
+        }
+    }
+    if (st[m].status != kConverged) return;
+    const uint32_t T = ocnt[rid];
     for (uint32_t q = tid; q <= T / 32; q += ST) bits[q] = 0u;
     __syncthreads();
     mark(0);
@@ -288,8 +300,13 @@ __global__ void __launch_bounds__(ST, 1) k_var_scan(const BlockState* st, const 
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             const uint32_t j = tid + (h + k) * ST;
-            pv[k] = j < T ? P[j] : 0xffffu;
-            x[k] = j < T ? X[j] : 0.0;
+            if (h == 0) {
+                pv[k] = j < T ? pv0[k] : 0xffffu;
+                x[k] = x0[k];
+            } else {
+                pv[k] = j < T ? P[j] : 0xffffu;
+                x[k] = j < T ? X[j] : 0.0;
+            }
         }
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
