@@ -371,13 +371,21 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
         }
     } else {  // fp32 per-point arithmetic: per-thread fp32 partial sums (PPT points), fp64 beyond
         float fs = 0.0f, fh = 0.0f;
+        constexpr int WB = 8;  // T32 loads in flight per thread
         if (FAM == kFrank) {
             const FrankThetaF f(theta);
-#pragma unroll 4
-            for (int k = 0; k < PPT; ++k) {
-                const uint32_t i = k * FT + threadIdx.x;
+            for (int k0 = 0; k0 < PPT; k0 += WB) {
+              TI pb[WB];
+#pragma unroll
+              for (int u = 0; u < WB; ++u) {
+                const uint32_t i = (k0 + u) * FT + threadIdx.x;
+                if (i < cnt) pb[u] = Tb[i];
+              }
+#pragma unroll
+              for (int u = 0; u < WB; ++u) {
+                const uint32_t i = (k0 + u) * FT + threadIdx.x;
                 if (i < cnt) {
-                    const TI p = Tb[i];
+                    const TI p = pb[u];
                     float uv, uc, vv, vc;
                     frank_unedge(p.x, uv, uc);
                     frank_unedge(p.y, vv, vc);
@@ -400,19 +408,27 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
                     fs += f.neg ? -s : s;
                     fh += h;
                 }
+              }
             }
         } else {
             const GumbelThetaF g(theta);
-#pragma unroll 4
-            for (int k = 0; k < PPT; ++k) {
-                const uint32_t i = k * FT + threadIdx.x;
+            for (int k0 = 0; k0 < PPT; k0 += WB) {
+              TI pb[WB];
+#pragma unroll
+              for (int u = 0; u < WB; ++u) {
+                const uint32_t i = (k0 + u) * FT + threadIdx.x;
+                if (i < cnt) pb[u] = Tb[i];
+              }
+#pragma unroll
+              for (int u = 0; u < WB; ++u) {
+                const uint32_t i = (k0 + u) * FT + threadIdx.x;
                 if (i < cnt) {
-                    const TI p = Tb[i];
                     float s, h;
-                    gumbel_sh_f(p.x, p.y, g, s, h);
+                    gumbel_sh_f(pb[u].x, pb[u].y, g, s, h);
                     fs += s;
                     fh += h;
                 }
+              }
             }
         }
         v[0] = fs;
