@@ -182,7 +182,10 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
     const double* gt = gtab ? gtab + 4 * goff[m] : nullptr;  // 4 doubles per rank entry
     const bool rt = R.routed && R.routed[m];
     double v[2] = {0.0, 0.0};
-    constexpr int U = 4;  // points per thread in flight
+#ifndef PCB_U_PREP
+#define PCB_U_PREP 4
+#endif
+    constexpr int U = PCB_U_PREP;  // points per thread in flight
     for (int k0 = 0; k0 < PPT; k0 += U) {
         double uu[U], ww[U], gx[U], gy[U];
         uint32_t ra[U], rb[U];

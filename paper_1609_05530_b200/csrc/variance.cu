@@ -129,7 +129,13 @@ __global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState
     const bool rt = R.routed && R.routed[m];
     const uint64_t c1 = rt ? slot_index(R, nseg, 0, m, 0u) : 0, c2 = rt ? slot_index(R, nseg, 1, m, 0u) : 0;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
-    constexpr int U = (FAM == kGaussian && MODE == kFromTable) ? 4 : 2;  // points per thread in flight
+#ifndef PCB_U_VPG
+#define PCB_U_VPG 4
+#endif
+#ifndef PCB_U_VP
+#define PCB_U_VP 2
+#endif
+    constexpr int U = (FAM == kGaussian && MODE == kFromTable) ? PCB_U_VPG : PCB_U_VP;  // points in flight
     for (int k0 = 0; k0 < PPT; k0 += U) {
         unsigned long long p1[U], p2[U];  // packed ranks (by-row blocks)
         uint32_t w1[U], w2[U];            // route words (routed blocks)
@@ -407,7 +413,10 @@ __global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* seg
     const double inv_n = 1.0 / static_cast<double>(S.n);
     const uint32_t base = (tile - S.tile0) * FTILE;
     double v[1] = {0.0};
-    constexpr int U = 4;
+#ifndef PCB_U_FINAL
+#define PCB_U_FINAL 4
+#endif
+    constexpr int U = PCB_U_FINAL;
     for (int k0 = 0; k0 < PPT; k0 += U) {
         uint32_t r1[U], r2[U];
         double zz[U];
