@@ -168,6 +168,15 @@ int pcb_fit_parallel(pcb_context* ctx, int family, int precision, const double* 
 int pcb_sample(pcb_context* ctx, int family, double theta, uint64_t n_total, uint64_t n_blocks_total,
                uint64_t first_block, uint64_t last_block, uint64_t base_seed, double* col1, double* col2);
 
+/* -------------------------------------------------------------- sim_study */
+/* rel_l1 / rel_l2 (Eq. 19-20): relative L1 and L2 distance
+ * of c(.; theta_b) from c(.; theta_a) over the unit square by a tensor
+ * Gauss-Legendre rule with quad_nodes^2 interior nodes (quadrature.hpp:22-78),
+ * c = exp(log_pdf) with the reference's clamp and clip (copula.hpp:293-313).
+ * Equal thetas give exactly 0. */
+int pcb_rel_error(pcb_context* ctx, int family, double theta_a, double theta_b, int quad_nodes, double* rel_l1,
+                  double* rel_l2);
+
 /* ------------------------------------------------------------- measurement */
 /* DFMA-loop microbenchmark: sustained FP64 instructions/s of this device
  * (the FP64 roofline denominator). */

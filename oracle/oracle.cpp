@@ -40,7 +40,57 @@ double debye1_restated(double x) {
     return simpson_rec(f, 0.0, x, fa, fm, fb, whole, 1e-13 * std::max(1.0, x), 48) / x;
 }
 
+// quadrature.hpp:22-62 restated: n-point Gauss-Legendre on (0, 1)
+void gauss_legendre01_restated(int n, std::vector<double>& x, std::vector<double>& w) {
+    x.assign(n, 0.0);
+    w.assign(n, 0.0);
+    const double pi = 3.14159265358979323846;
+    for (int i = 0; i < (n + 1) / 2; ++i) {
+        double z = std::cos(pi * (i + 0.75) / (n + 0.5)), dp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = z;
+            for (int j = 2; j <= n; ++j) {
+                const double p2 = ((2.0 * j - 1.0) * z * p1 - (j - 1.0) * p0) / j;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = n * (z * p1 - p0) / (z * z - 1.0);
+            const double step = p1 / dp;
+            z -= step;
+            if (std::fabs(step) < 1e-15) break;
+        }
+        x[i] = -z;
+        x[n - 1 - i] = z;
+        w[i] = w[n - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+    }
+    if (n % 2 == 1) x[n / 2] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        x[i] = 0.5 * (x[i] + 1.0);
+        w[i] *= 0.5;
+    }
+}
+
 struct RestatedMath {
+    // SPEC.md:362-374 sums over the tensor rule (quadrature.hpp:66-78 order:
+    // row sums over j, then the weighted sum over rows i)
+    static void rel_sums(int fam, double ta, double tb, int n, double out[4]) {
+        std::vector<double> x, w;
+        gauss_legendre01_restated(n, x, w);
+        for (int k = 0; k < 4; ++k) out[k] = 0.0;
+        for (int i = 0; i < n; ++i) {
+            double row[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int j = 0; j < n; ++j) {
+                const double fa = std::exp(oracle::log_density(fam, ta, x[i], x[j]));
+                const double fb = std::exp(oracle::log_density(fam, tb, x[i], x[j]));
+                const double d = fa - fb;
+                row[0] += w[j] * std::fabs(d);
+                row[1] += w[j] * (d * d);
+                row[2] += w[j] * fa;
+                row[3] += w[j] * (fa * fa);
+            }
+            for (int k = 0; k < 4; ++k) out[k] += w[i] * row[k];
+        }
+    }
     static void rank_column(const double* x, size_t n, double* u) { oracle::rank_column_restated(x, n, u); }
     static double log_density(int fam, double t, double u, double v) { return oracle::log_density(fam, t, u, v); }
     static oracle::PointDerivs derivs(int fam, double t, double u, double v) {

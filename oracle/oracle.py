@@ -203,6 +203,12 @@ class Lib:
         self._call("debye1", x, C.byref(out))
         return out.value
 
+    def rel_error(self, fam, ta, tb, nodes=200):
+        """(rel_l1, rel_l2) of SPEC.md:362-374 by the tensor Gauss-Legendre rule."""
+        out = np.zeros(2, np.float64)
+        self._call("rel_error", fam, C.c_double(ta), C.c_double(tb), nodes, _dp(out), None)
+        return float(out[0]), float(out[1])
+
     # ---- generators
     def sample_blocks(self, fam, theta, n_total, k, offsets, first, last, base_seed=BASE_SEED, workers=None):
         assert self.p == "orc_"

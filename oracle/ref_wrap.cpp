@@ -44,6 +44,26 @@ struct RefMath {
         return derivs(fam, t, u, v);
     }
     static double debye1(double x) { return parcop::debye1(x); }
+    // the reference's own tensor quadrature (quadrature.hpp:66-78) of its pdf (copula.hpp:313)
+    static void rel_sums(int fam, double ta, double tb, int n, double out[4]) {
+        const parcop::CopulaModel a{fam_of(fam), ta}, b{fam_of(fam), tb};
+        auto pa = [&](double u, double v) { return parcop::pdf(a, parcop::UnitPair{u, v}); };
+        auto pb = [&](double u, double v) { return parcop::pdf(b, parcop::UnitPair{u, v}); };
+        out[0] = parcop::integrate_unit_square([&](double u, double v) { return std::fabs(pa(u, v) - pb(u, v)); }, n);
+        out[1] = parcop::integrate_unit_square(
+            [&](double u, double v) {
+                const double d = pa(u, v) - pb(u, v);
+                return d * d;
+            },
+            n);
+        out[2] = parcop::integrate_unit_square(pa, n);
+        out[3] = parcop::integrate_unit_square(
+            [&](double u, double v) {
+                const double f = pa(u, v);
+                return f * f;
+            },
+            n);
+    }
 };
 
 }  // namespace

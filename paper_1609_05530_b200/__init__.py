@@ -10,3 +10,6 @@ from .parcop import (  # noqa: F401
     family_from_string, fit, fit_blocks, fit_parallel, normalized_ranks, partition, pseudo_loglik, sample_matrix,
     validate_data,
 )
+from .study import (  # noqa: F401,E402
+    ReplicateRow, SimConfig, SimReport, est_bias, est_mse, mix_seed, rel_error, rel_l1, rel_l2, run_study,
+)

@@ -18,7 +18,7 @@ SYMBOLS = (
     "pcb_create", "pcb_destroy", "pcb_last_error", "pcb_abi_version", "pcb_set_stream", "pcb_launch_count",
     "pcb_stage_times", "pcb_trim", "pcb_normalized_ranks", "pcb_pseudo_loglik", "pcb_fit",
     "pcb_asymptotic_variance", "pcb_partition", "pcb_combine", "pcb_fit_blocks", "pcb_fit_parallel", "pcb_sample",
-    "pcb_measure_fp64_peak",
+    "pcb_measure_fp64_peak", "pcb_rel_error",
 )
 
 PCB_OK, PCB_E_INVALID, PCB_E_DOMAIN, PCB_E_CONVERGENCE, PCB_E_CUDA = 0, 2, 3, 4, 5
@@ -79,6 +79,7 @@ def load():
         "pcb_fit_parallel": ([vp, i, i, vp, vp, u64, u64, i, vp, vp, P(CombinedC)], i),
         "pcb_sample": ([vp, i, d, u64, u64, u64, u64, u64, vp, vp], i),
         "pcb_measure_fp64_peak": ([vp, P(d)], i),
+        "pcb_rel_error": ([vp, i, d, d, i, P(d), P(d)], i),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

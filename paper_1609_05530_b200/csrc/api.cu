@@ -586,6 +586,21 @@ int pcb_sample(pcb_context* ctx, int family, double theta, uint64_t n_total, uin
     });
 }
 
+int pcb_rel_error(pcb_context* ctx, int family, double theta_a, double theta_b, int quad_nodes, double* rel_l1,
+                  double* rel_l2) {
+    return guarded(ctx, [&] {
+        check_family(family);
+        if (!theta_in_domain(family, theta_a) || !theta_in_domain(family, theta_b))
+            throw pcb::Error(PCB_E_DOMAIN, "theta outside the family domain");
+        if (quad_nodes < 1 || quad_nodes > 65536) throw pcb::Error(PCB_E_INVALID, "rel_error: quad_nodes out of range");
+        if (!rel_l1 || !rel_l2) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        double s[4];
+        pcb::run_rel_error(ctx->c, family, theta_a, theta_b, quad_nodes, s);
+        *rel_l1 = s[0] / s[2];                        // Eq. 19
+        *rel_l2 = std::sqrt(s[1]) / std::sqrt(s[3]);  // Eq. 20
+    });
+}
+
 int pcb_measure_fp64_peak(pcb_context* ctx, double* v) {
     return guarded(ctx, [&] {
         if (!v) throw pcb::Error(PCB_E_INVALID, "NULL pointer");

@@ -179,6 +179,10 @@ void run_combine(Ctx& c, const void* d_records, uint64_t n, double* d_weights, d
 void run_sample(Ctx& c, int family, double theta, uint64_t n_total, uint64_t k_total, uint64_t first,
                 uint64_t last, uint64_t base_seed, double* d_col1, double* d_col2);
 
+// Eq. 19-20 sums over the tensor Gauss-Legendre grid: out4 = {sum |fa-fb|,
+// sum (fa-fb)^2, sum fa, sum fa^2} (weighted)
+void run_rel_error(Ctx& c, int family, double ta, double tb, int nodes, double out4[4]);
+void gauss_legendre01(int n, std::vector<double>& x, std::vector<double>& w);
 void run_strided_gather(Ctx& c, const double* src, uint64_t n_rows, uint64_t m, double* dst);
 
 double run_fp64_peak(Ctx& c);

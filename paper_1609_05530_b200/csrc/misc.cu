@@ -54,6 +54,42 @@ __global__ void __launch_bounds__(1024) k_combine(const RecordIn* r, uint64_t n,
     }
 }
 
+// --------------------------------------------------- relative L1 / L2 errors
+// SPEC.md:362-374 (Eq. 19-20): tensor Gauss-Legendre over the unit square of
+// c(.; theta_a) and c(.; theta_b) (quadrature.hpp:66-78 layout: per row i,
+// sum_j w_j f(x_i, y_j); then sum_i w_i row_i). One CTA per row; the rows are
+// combined by one thread in row order (deterministic).
+__device__ __forceinline__ double pdf_dev(int fam, double t, double u, double v) {  // copula.hpp:293-313
+    return exp(clip_log(logc_any(fam, t, clamp_unit(u), clamp_unit(v))));
+}
+
+__global__ void __launch_bounds__(256) k_rel_rows(int fam, double ta, double tb, const double* __restrict__ x,
+                                                 const double* __restrict__ w, int n, double* rows) {
+    const int i = blockIdx.x;
+    const double xi = x[i];
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const double fa = pdf_dev(fam, ta, xi, x[j]);
+        const double fb = pdf_dev(fam, tb, xi, x[j]);
+        const double d = fa - fb;
+        v[0] += w[j] * fabs(d);
+        v[1] += w[j] * (d * d);
+        v[2] += w[j] * fa;
+        v[3] += w[j] * (fa * fa);
+    }
+    __shared__ double sh[(256 / 32) * 4];
+    block_sum<4>(v, sh);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 4; ++k) rows[4 * i + k] = v[k];
+}
+
+__global__ void k_rel_total(const double* w, const double* rows, int n, double* out) {
+    if (threadIdx.x >= 4) return;
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += w[i] * rows[4 * i + threadIdx.x];
+    out[threadIdx.x] = t;
+}
+
 // ------------------------------------------------------------------ sampler
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {  // rng.hpp:15-20
     z += 0x9e3779b97f4a7c15ull;
@@ -170,6 +206,56 @@ __global__ void k_dfma(double* out, int iters) {
 void run_combine(Ctx& c, const void* d_records, uint64_t n, double* d_weights, double* d_out3) {
     k_combine<<<1, 1024, 0, c.stream>>>(static_cast<const RecordIn*>(d_records), n, d_weights, d_out3);
     c.count_launch();
+}
+
+// n-point Gauss-Legendre rule on (0, 1) (quadrature.hpp:22-62): Newton on
+// P_n from cos(pi (i + 0.75) / (n + 0.5)), w = 2 / ((1 - x^2) P_n'(x)^2), mapped.
+void gauss_legendre01(int n, std::vector<double>& x, std::vector<double>& w) {
+    x.assign(n, 0.0);
+    w.assign(n, 0.0);
+    const double pi = 3.14159265358979323846;
+    for (int i = 0; i < (n + 1) / 2; ++i) {
+        double z = std::cos(pi * (i + 0.75) / (n + 0.5));
+        double dp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = z;
+            for (int j = 2; j <= n; ++j) {
+                const double p2 = ((2.0 * j - 1.0) * z * p1 - (j - 1.0) * p0) / j;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = n * (z * p1 - p0) / (z * z - 1.0);
+            const double step = p1 / dp;
+            z -= step;
+            if (std::fabs(step) < 1e-15) break;
+        }
+        const double wt = 2.0 / ((1.0 - z * z) * dp * dp);
+        x[i] = -z;
+        x[n - 1 - i] = z;
+        w[i] = wt;
+        w[n - 1 - i] = wt;
+    }
+    if (n % 2 == 1) x[n / 2] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        x[i] = 0.5 * (x[i] + 1.0);
+        w[i] *= 0.5;
+    }
+}
+
+void run_rel_error(Ctx& c, int family, double ta, double tb, int nodes, double out4[4]) {
+    std::vector<double> hx, hw;
+    gauss_legendre01(nodes, hx, hw);
+    auto* d_x = c.ws.get_t<double>("rel.x", nodes);
+    auto* d_w = c.ws.get_t<double>("rel.w", nodes);
+    auto* rows = c.ws.get_t<double>("rel.rows", 4 * static_cast<size_t>(nodes));
+    auto* d_out = c.ws.get_t<double>("rel.out", 4);
+    PCB_CUDA(cudaMemcpyAsync(d_x, hx.data(), nodes * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    PCB_CUDA(cudaMemcpyAsync(d_w, hw.data(), nodes * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    k_rel_rows<<<nodes, 256, 0, c.stream>>>(family, ta, tb, d_x, d_w, nodes, rows);
+    k_rel_total<<<1, 32, 0, c.stream>>>(d_w, rows, nodes, d_out);
+    c.count_launch(2);
+    PCB_CUDA(cudaMemcpyAsync(out4, d_out, 4 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    PCB_CUDA(cudaStreamSynchronize(c.stream));
 }
 
 void run_sample(Ctx& c, int family, double theta, uint64_t n_total, uint64_t k_total, uint64_t first, uint64_t last,
