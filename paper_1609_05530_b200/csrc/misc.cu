@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) k_rel_rows(int fam, double ta, double tb,
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
         const double fa = pdf_dev(fam, ta, xi, x[j]);
-        const double fb = pdf_dev(fam, tb, xi, x[j]);
+        const double fb = ta == tb ? fa : pdf_dev(fam, tb, xi, x[j]);  // exactly 0 at equal parameters
         const double d = fa - fb;
         v[0] += w[j] * fabs(d);
         v[1] += w[j] * (d * d);

@@ -108,7 +108,7 @@ def test_run_study_m1_identities_and_reproducibility(ctx):
 def test_cli_split_fit_m1_equals_fit(ctx, tmp_path, capsys):
     X = pcb.sample_matrix(1, 5.0, 5000, 1, ctx=ctx)
     p = tmp_path / "x.csv"
-    p.write_text("\n".join(f"{a!r},{b!r}" for a, b in zip(X.col1, X.col2)) + "\n")
+    p.write_text("\n".join(f"{float(a)!r},{float(b)!r}" for a, b in zip(X.col1, X.col2)) + "\n")
     assert cli.main(["fit", str(p), "--family", "frank"]) == 0
     fit_line = capsys.readouterr().out.strip().splitlines()[-1]
     out = tmp_path / "blocks.csv"
