@@ -217,5 +217,20 @@ inline CombinedResult fit_parallel(CopulaFamily f, const DataMatrix& x, std::siz
     return out;
 }
 
+// sim_study rel_l1 / rel_l2, tensor Gauss-Legendre on device
+inline double rel_l1(CopulaFamily f, double theta_a, double theta_b, int quad_nodes = 200) {
+    double l1 = 0.0, l2 = 0.0;
+    pcb_context* c = detail::ctx();
+    detail::rethrow(c, pcb_rel_error(c, static_cast<int>(f), theta_a, theta_b, quad_nodes, &l1, &l2));
+    return l1;
+}
+
+inline double rel_l2(CopulaFamily f, double theta_a, double theta_b, int quad_nodes = 200) {
+    double l1 = 0.0, l2 = 0.0;
+    pcb_context* c = detail::ctx();
+    detail::rethrow(c, pcb_rel_error(c, static_cast<int>(f), theta_a, theta_b, quad_nodes, &l1, &l2));
+    return l2;
+}
+
 }  // namespace b200
 }  // namespace parcop

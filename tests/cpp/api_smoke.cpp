@@ -61,5 +61,7 @@ int main() {
         threw = true;
     }
     std::printf("theta domain_error %s\n", threw ? "ok" : "FAIL");
+    const double l1 = rel_l1(CopulaFamily::Frank, 5.0, 5.2, 64), l0 = rel_l2(CopulaFamily::Frank, 5.0, 5.0, 64);
+    std::printf("rel_error %s l1=%.12g\n", l1 > 0.0 && l1 < 1.0 && l0 == 0.0 ? "ok" : "FAIL", l1);
     return 0;
 }
