@@ -735,8 +735,8 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
         // Gaussian: the rank table (x, exp(x^2/2)) replaces T; Gumbel re-reads
         // T (coalesced) rather than gathering 32-byte table entries at random
         v.gtab = fam == kGaussian ? gtab : nullptr;
-        v.T64 = (!v.gtab && (fam == kGaussian || (fam == kGumbel && !fp32T))) ? static_cast<const double2*>(T)
-                                                                               : nullptr;
+        // Frank's fp64 T is (u, v) itself; Gumbel's is (ln(-ln u), ln(-ln v))
+        v.T64 = (!v.gtab && (fam == kGaussian || !fp32T)) ? static_cast<const double2*>(T) : nullptr;
         v.goff = goff;
         v.partials = part;
         v.tickets = tick;

@@ -61,7 +61,9 @@ struct ThetaOf<kGumbel> {
 };
 
 // Where a point's theta-independent transforms come from
-enum { kFromU = 0, kFromT64 = 1, kFromTable = 2 };
+//   kFromTU: T carries u too (Frank: T = (u, v) exactly; Gumbel: T = (ln x,
+//   ln y) and u = exp(-x), within an ulp or two), so no rank gathers
+enum { kFromU = 0, kFromT64 = 1, kFromTable = 2, kFromTU = 3 };
 
 template <int FAM, int MODE>
 __device__ __forceinline__ PointFull eval_point(const typename ThetaOf<FAM>::type& th, double u, double w,
@@ -75,7 +77,7 @@ __device__ __forceinline__ PointFull eval_point(const typename ThetaOf<FAM>::typ
     } else {
         if constexpr (MODE == kFromTable)
             return gumbel_full_t(ta[0].x, tb[0].x, ta[0].y, tb[0].y, ta[1].x, tb[1].x, ta[1].y, tb[1].y, th);
-        else if constexpr (MODE == kFromT64) return gumbel_full_l(u, w, t64.x, t64.y, th);
+        else if constexpr (MODE == kFromT64 || MODE == kFromTU) return gumbel_full_l(u, w, t64.x, t64.y, th);
         else return gumbel_full(u, w, th);
     }
 }
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState
                     uu[j] = u1[row];
                     ww[j] = u2[row];
                 }
-                if (MODE == kFromT64) tt[j] = T64[row];
+                if (MODE == kFromT64 || MODE == kFromTU) tt[j] = T64[row];
             }
         }
 #pragma unroll
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState
             if (!rt) {
                 q1[j] = rank_r2(p1[j]);
                 q2[j] = rank_r2(p2[j]);
-            } else if (!u1) {
+            } else if (!u1 && MODE != kFromTU) {
                 q1[j] = R.r2s[c1 + (w1[j] >> 16) * R.rcap + (w1[j] & 0xffffu)];
                 q2[j] = R.r2s[c2 + (w2[j] >> 16) * R.rcap + (w2[j] & 0xffffu)];
             }
@@ -192,10 +194,21 @@ __global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState
             const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
             if (i >= S.n) continue;
             const uint64_t row = S.begin + i;
-            double u = u1 ? uu[j] : __dmul_rn(0.5 * static_cast<double>(q1[j]), scale);
-            double w = u1 ? ww[j] : __dmul_rn(0.5 * static_cast<double>(q2[j]), scale);
-            u = clamp_unit(u);
-            w = clamp_unit(w);
+            double u, w;
+            if constexpr (MODE == kFromTU) {
+                if constexpr (FAM == kFrank) {
+                    u = tt[j].x;
+                    w = tt[j].y;
+                } else {
+                    u = exp(-exp(tt[j].x));
+                    w = exp(-exp(tt[j].y));
+                }
+            } else {
+                u = u1 ? uu[j] : __dmul_rn(0.5 * static_cast<double>(q1[j]), scale);
+                w = u1 ? ww[j] : __dmul_rn(0.5 * static_cast<double>(q2[j]), scale);
+                u = clamp_unit(u);
+                w = clamp_unit(w);
+            }
             const PointFull p = eval_point<FAM, MODE>(th, u, w, tt[j], ta[j], tb[j]);
             zb[row] = p.score;
             if (rt) {  // cross_j to (owner, slot) of the rank stage's route
@@ -571,6 +584,7 @@ void launch_var_point(Ctx& c, const VarIO& v, double* zb, double* Ag, double* xr
     k_var_point<FAM, MODE><<<v.tiles, FT, 0, c.stream>>>(v.st, v.segs, K, v.rank->ref(), v.u1, v.u2, v.T64, v.gtab, \
                                                          v.goff, v.n_rows, zb, Ag, xr, v.partials, v.tickets)
     if (FAM != kFrank && v.gtab) PCB_VAR_POINT(kFromTable);
+    else if (FAM != kGaussian && v.T64 && !v.u1 && !std::getenv("PCB_VAR_NO_TU")) PCB_VAR_POINT(kFromTU);
     else if (FAM != kFrank && v.T64) PCB_VAR_POINT(kFromT64);
     else PCB_VAR_POINT(kFromU);
 #undef PCB_VAR_POINT

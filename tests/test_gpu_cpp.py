@@ -16,6 +16,6 @@ def test_cpp_api_smoke():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
     lines = out.stdout.strip().splitlines()
-    assert len(lines) == 7, out.stdout
+    assert len(lines) == 8, out.stdout
     for line in lines:
         assert " ok" in line, out.stdout
