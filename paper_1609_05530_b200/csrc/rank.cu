@@ -394,7 +394,7 @@ inline ClusterPlan plan_for(uint64_t nmax, int cl) {
     ClusterPlan p;
     p.cl = cl;
     p.s = slice_of(nmax, cl);
-    const uint32_t slack = std::max<uint32_t>(256u, static_cast<uint32_t>(6.0 * std::sqrt(static_cast<double>(p.s))));
+    const uint32_t slack = std::max<uint32_t>(256u, static_cast<uint32_t>(5.5 * std::sqrt(static_cast<double>(p.s))));
     p.rcap = (p.s + slack + 31u) & ~31u;
     uint32_t lg = 1;
     while ((2u << lg) <= std::max<uint32_t>(2u, p.s)) ++lg;  // NBL = largest power of two <= S (>= 2)
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
                                                        uint32_t* r2s_g, uint16_t* posl_g, uint32_t* ocnt, uint32_t K,
                                                        int32_t* fb,
                                                        int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
-                                                       unsigned long long* prof) {
+                                                       int tail, unsigned long long* prof) {
     namespace cg = cooperative_groups;
     long long t_prev = clock64();
     auto mark = [&](int k) {  // optional phase timing (PCB_RANK_PROFILE): thread 0's clock deltas
@@ -504,7 +504,10 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     const uint32_t x_off = static_cast<uint32_t>((reinterpret_cast<uint64_t>(x + a) - g_lo) >> 3);
     const uint64_t g_hi = (reinterpret_cast<uint64_t>(x + e) + 15ull) & ~15ull;
     const bool staged = e > a;
-    const double* xs = reinterpret_cast<const double*>(smem) + x_off - a;  // xs[i] == x[i] for i in [a, e)
+    // tail mode: the slice sits after the receive buffer (where the sort's
+    // arrays go later), so it stays readable while peers fill the buffer
+    unsigned char* stage_at = tail ? smem + static_cast<size_t>(RCAP) * 8 : smem;
+    const double* xs = reinterpret_cast<const double*>(stage_at) + x_off - a;  // xs[i] == x[i] for i in [a, e)
     if (tid == 0 && staged) {
         const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
         const uint32_t bytes = static_cast<uint32_t>(g_hi - g_lo);
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                static_cast<uint32_t>(__cvta_generic_to_shared(stage_at))),
             "l"(g_lo), "r"(bytes), "r"(mb)
             : "memory");
     }
@@ -713,6 +716,19 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     // The owner never needs the row: its outputs are written per receive slot
     // and the row finds them through route[row] = (owner, slot).
     constexpr int SB = 8;  // slice reloads in flight per thread (L2 hits)
+    if (tail) {
+#pragma unroll
+      for (int k = 0; k < EMAX; ++k) {
+        const uint32_t i = a + k * CT + tid;
+        if (i < e) {
+            const unsigned long long kk = order_key(xs[i]);
+            const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
+            const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
+            route[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = (d << 16) | slot;
+            *cluster.map_shared_rank(recv_key + slot, d) = kk;
+        }
+      }
+    } else
 #pragma unroll
     for (int h = 0; h < EMAX; h += SB) {
       if (a + h * CT >= e) break;
@@ -807,13 +823,22 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
 
 void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, uint32_t njobs, const double* c0,
                          const double* c1, uint64_t n_rows, RankOut& out, int32_t* fb, int32_t* bad) {
+    // tail mode when the slice fits after the receive buffer
+    cudaFuncAttributes fa;
+    PCB_CUDA(cudaFuncGetAttributes(&fa, k_rank_cluster));
+    int optin = 0;
+    PCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+    const size_t tail_bytes = static_cast<size_t>(p.rcap) * 8 + (static_cast<size_t>(p.s) + 2) * 8 + 16;
+    const int tail = (tail_bytes + fa.sharedSizeBytes <= static_cast<size_t>(optin) && !getenv_flag("PCB_RANK_NO_TAIL"))
+                         ? 1 : 0;
+    const size_t smem = tail ? std::max(p.smem, tail_bytes) : p.smem;
     PCB_CUDA(cudaFuncSetAttribute(k_rank_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(p.smem)));
+                                  static_cast<int>(smem)));
     if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(k_rank_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(njobs * static_cast<uint32_t>(p.cl));
     cfg.blockDim = dim3(CT);
-    cfg.dynamicSmemBytes = p.smem;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -829,7 +854,7 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
     }
     PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, out.rp, out.route, out.r2s, out.posl,
                                 out.ocnt,
-                                njobs / 2, fb, bad, p.cl, p.rcap, p.lg_nbl, prof));
+                                njobs / 2, fb, bad, p.cl, p.rcap, p.lg_nbl, tail, prof));
     if (prof) {
         unsigned long long h[8];
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
