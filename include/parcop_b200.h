@@ -177,6 +177,21 @@ int pcb_sample(pcb_context* ctx, int family, double theta, uint64_t n_total, uin
 int pcb_rel_error(pcb_context* ctx, int family, double theta_a, double theta_b, int quad_nodes, double* rel_l1,
                   double* rel_l2);
 
+/* ----------------------------------------------------- CDF and dependence */
+/* cdf (copula.hpp:273-290; Gaussian through bvn_cdf, normal.hpp:84-166) at n
+ * points (u, v clamped like the reference). */
+int pcb_cdf(pcb_context* ctx, int family, double theta, const double* u, const double* v, uint64_t n, double* out);
+/* spearman_rho of the model: 12 * int C - 3 by the tensor
+ * Gauss-Legendre rule with quad_nodes^2 nodes. */
+int pcb_spearman_rho(pcb_context* ctx, int family, double theta, int quad_nodes, double* rho);
+/* empirical Kendall tau of each segment's first min(n_m, m_max) rows (the
+ * fit's SPEC init; m_max <= 8192): 1 - 2 * discordant / pairs. */
+int pcb_kendall_tau(pcb_context* ctx, const double* u1, const double* u2, uint64_t n_rows,
+                    const uint64_t* seg_offsets, uint64_t n_seg, uint64_t m_max, double* tau);
+/* kendall_tau of the model and inverse_tau, host scalars */
+int pcb_model_kendall_tau(int family, double theta, double* tau);
+int pcb_inverse_tau(int family, double tau, double* theta);
+
 /* ------------------------------------------------------------- measurement */
 /* DFMA-loop microbenchmark: sustained FP64 instructions/s of this device
  * (the FP64 roofline denominator). */

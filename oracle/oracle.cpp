@@ -70,7 +70,116 @@ void gauss_legendre01_restated(int n, std::vector<double>& x, std::vector<double
     }
 }
 
+// normal.hpp:97-155 restated (bvn_upper over the 6/12/20-node rules of bvn_rule)
+double bvn_upper_restated(double h, double k, double r) {
+    const double twopi = 2.0 * 3.14159265358979323846;
+    const double ar = std::fabs(r);
+    const int nn = ar < 0.3 ? 6 : (ar < 0.75 ? 12 : 20);  // bvn_rule, normal.hpp:84-91
+    std::vector<double> x(nn), w(nn);
+    {  // recompute on [-1, 1] exactly as quadrature.hpp:22-55 (before its (0, 1) map)
+        const double pi = 3.14159265358979323846;
+        for (int i = 0; i < (nn + 1) / 2; ++i) {
+            double z = std::cos(pi * (i + 0.75) / (nn + 0.5)), dp = 0.0;
+            for (int it = 0; it < 100; ++it) {
+                double p0 = 1.0, p1 = z;
+                for (int j = 2; j <= nn; ++j) {
+                    const double p2 = ((2.0 * j - 1.0) * z * p1 - (j - 1.0) * p0) / j;
+                    p0 = p1;
+                    p1 = p2;
+                }
+                dp = nn * (z * p1 - p0) / (z * z - 1.0);
+                const double step = p1 / dp;
+                z -= step;
+                if (std::fabs(step) < 1e-15) break;
+            }
+            x[i] = -z;
+            x[nn - 1 - i] = z;
+            w[i] = w[nn - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+        }
+        if (nn % 2 == 1) x[nn / 2] = 0.0;
+    }
+    double hk = h * k, bvn = 0.0;
+    if (ar < 0.925) {
+        if (ar > 0.0) {
+            const double hs = 0.5 * (h * h + k * k), asr = std::asin(r);
+            for (int i = 0; i < nn; ++i) {
+                const double sn = std::sin(0.5 * asr * (x[i] + 1.0));
+                bvn += w[i] * std::exp((sn * hk - hs) / (1.0 - sn * sn));
+            }
+            bvn *= asr / (2.0 * twopi);
+        }
+        bvn += oracle::phi_cdf(-h) * oracle::phi_cdf(-k);
+    } else {
+        if (r < 0.0) {
+            k = -k;
+            hk = -hk;
+        }
+        if (ar < 1.0) {
+            const double as = (1.0 - r) * (1.0 + r);
+            double a = std::sqrt(as);
+            const double bs = (h - k) * (h - k), cc = (4.0 - hk) / 8.0, dd = (12.0 - hk) / 16.0;
+            double asr = -0.5 * (bs / as + hk);
+            if (asr > -100.0)
+                bvn = a * std::exp(asr) * (1.0 - cc * (bs - as) * (1.0 - dd * bs / 5.0) / 3.0 + cc * dd * as * as / 5.0);
+            if (-hk < 100.0) {
+                const double bb = std::sqrt(bs);
+                bvn -= std::exp(-0.5 * hk) * std::sqrt(twopi) * oracle::phi_cdf(-bb / a) * bb *
+                       (1.0 - cc * bs * (1.0 - dd * bs / 5.0) / 3.0);
+            }
+            a *= 0.5;
+            for (int i = 0; i < nn; ++i) {
+                const double t = a * (x[i] + 1.0), xs = t * t;
+                asr = -0.5 * (bs / xs + hk);
+                if (asr > -100.0) {
+                    const double rs = std::sqrt(1.0 - xs);
+                    bvn += a * w[i] * std::exp(asr) *
+                           (std::exp(-hk * (1.0 - rs) / (2.0 * (1.0 + rs))) / rs - (1.0 + cc * xs * (1.0 + dd * xs)));
+                }
+            }
+            bvn = -bvn / twopi;
+        }
+        if (r > 0.0) {
+            bvn += oracle::phi_cdf(-std::max(h, k));
+        } else {
+            bvn = -bvn;
+            if (k > h) bvn += oracle::phi_cdf(k) - oracle::phi_cdf(h);
+        }
+    }
+    return std::clamp(bvn, 0.0, 1.0);
+}
+
+double frank_cdf_pos_restated(double u, double v, double t) {  // copula.hpp:174-181
+    const double lo = std::min(u, v), hi = std::max(u, v);
+    const double k2 = -t * (hi - lo);
+    const double b = std::expm1(-t * (1.0 - lo)) + std::exp(k2) * std::expm1(-t * lo);
+    return lo - (std::log(-b) - std::log(-std::expm1(-t))) / t;
+}
+
 struct RestatedMath {
+    // copula.hpp:273-290
+    static double cdf(int fam, double t, double u, double v) {
+        if (!oracle::theta_ok(fam, t)) throw std::domain_error("theta outside the family domain");
+        u = oracle::clamp01(u);
+        v = oracle::clamp01(v);
+        if (fam == 0) return bvn_upper_restated(-oracle::phi_inv(u), -oracle::phi_inv(v), t);
+        if (fam == 1) return t > 0.0 ? frank_cdf_pos_restated(u, v, t) : u - frank_cdf_pos_restated(u, 1.0 - v, -t);
+        const double lx = std::log(-std::log(u)), ly = std::log(-std::log(v));
+        const double a = t * lx, b = t * ly, m = std::max(a, b);
+        const double lnS = m + std::log(std::exp(a - m) + std::exp(b - m));
+        return std::exp(-std::exp(lnS / t));
+    }
+    // 12 int C - 3, same tensor rule order as rel_sums
+    static double spearman_rho(int fam, double t, int n) {
+        std::vector<double> x, w;
+        gauss_legendre01_restated(n, x, w);
+        double total = 0.0;
+        for (int i = 0; i < n; ++i) {
+            double row = 0.0;
+            for (int j = 0; j < n; ++j) row += w[j] * cdf(fam, t, x[i], x[j]);
+            total += w[i] * row;
+        }
+        return 12.0 * total - 3.0;
+    }
     // SPEC.md:362-374 sums over the tensor rule (quadrature.hpp:66-78 order:
     // row sums over j, then the weighted sum over rows i)
     static void rel_sums(int fam, double ta, double tb, int n, double out[4]) {

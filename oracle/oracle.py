@@ -203,6 +203,18 @@ class Lib:
         self._call("debye1", x, C.byref(out))
         return out.value
 
+    def cdf(self, fam, t, u, v):
+        u = np.ascontiguousarray(np.atleast_1d(u), np.float64)
+        v = np.ascontiguousarray(np.atleast_1d(v), np.float64)
+        out = np.empty_like(u)
+        self._call("cdf_vec", fam, C.c_double(t), _dp(u), _dp(v), len(u), _dp(out))
+        return out
+
+    def spearman_rho(self, fam, t, nodes=200):
+        out = C.c_double()
+        self._call("spearman_rho", fam, C.c_double(t), nodes, C.byref(out))
+        return out.value
+
     def rel_error(self, fam, ta, tb, nodes=200):
         """(rel_l1, rel_l2) of SPEC.md:362-374 by the tensor Gauss-Legendre rule."""
         out = np.zeros(2, np.float64)

@@ -44,6 +44,15 @@ struct RefMath {
         return derivs(fam, t, u, v);
     }
     static double debye1(double x) { return parcop::debye1(x); }
+    static double cdf(int fam, double t, double u, double v) {
+        return parcop::cdf(parcop::CopulaModel{fam_of(fam), t}, parcop::UnitPair{u, v});
+    }
+    static double spearman_rho(int fam, double t, int n) {
+        const parcop::CopulaModel mdl{fam_of(fam), t};
+        return 12.0 * parcop::integrate_unit_square(
+                          [&](double u, double v) { return parcop::cdf(mdl, parcop::UnitPair{u, v}); }, n) -
+               3.0;
+    }
     // the reference's own tensor quadrature (quadrature.hpp:66-78) of its pdf (copula.hpp:313)
     static void rel_sums(int fam, double ta, double tb, int n, double out[4]) {
         const parcop::CopulaModel a{fam_of(fam), ta}, b{fam_of(fam), tb};

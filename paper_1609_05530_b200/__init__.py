@@ -13,3 +13,4 @@ from .parcop import (  # noqa: F401
 from .study import (  # noqa: F401,E402
     ReplicateRow, SimConfig, SimReport, est_bias, est_mse, mix_seed, rel_error, rel_l1, rel_l2, run_study,
 )
+from .dependence import cdf, empirical_kendall_tau, inverse_tau, kendall_tau, spearman_rho  # noqa: F401,E402

@@ -18,7 +18,8 @@ SYMBOLS = (
     "pcb_create", "pcb_destroy", "pcb_last_error", "pcb_abi_version", "pcb_set_stream", "pcb_launch_count",
     "pcb_stage_times", "pcb_trim", "pcb_normalized_ranks", "pcb_pseudo_loglik", "pcb_fit",
     "pcb_asymptotic_variance", "pcb_partition", "pcb_combine", "pcb_fit_blocks", "pcb_fit_parallel", "pcb_sample",
-    "pcb_measure_fp64_peak", "pcb_rel_error",
+    "pcb_measure_fp64_peak", "pcb_rel_error", "pcb_cdf", "pcb_spearman_rho", "pcb_kendall_tau",
+    "pcb_model_kendall_tau", "pcb_inverse_tau",
 )
 
 PCB_OK, PCB_E_INVALID, PCB_E_DOMAIN, PCB_E_CONVERGENCE, PCB_E_CUDA = 0, 2, 3, 4, 5
@@ -80,6 +81,11 @@ def load():
         "pcb_sample": ([vp, i, d, u64, u64, u64, u64, u64, vp, vp], i),
         "pcb_measure_fp64_peak": ([vp, P(d)], i),
         "pcb_rel_error": ([vp, i, d, d, i, P(d), P(d)], i),
+        "pcb_cdf": ([vp, i, d, vp, vp, u64, vp], i),
+        "pcb_spearman_rho": ([vp, i, d, i, P(d)], i),
+        "pcb_kendall_tau": ([vp, vp, vp, u64, P(u64), u64, u64, vp], i),
+        "pcb_model_kendall_tau": ([i, d, P(d)], i),
+        "pcb_inverse_tau": ([i, d, P(d)], i),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

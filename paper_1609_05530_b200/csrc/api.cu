@@ -601,6 +601,105 @@ int pcb_rel_error(pcb_context* ctx, int family, double theta_a, double theta_b, 
     });
 }
 
+int pcb_cdf(pcb_context* ctx, int family, double theta, const double* u, const double* v, uint64_t n, double* out) {
+    return guarded(ctx, [&] {
+        pcb::Ctx& c = ctx->c;
+        check_family(family);
+        if (!theta_in_domain(family, theta)) throw pcb::Error(PCB_E_DOMAIN, "theta outside the family domain");
+        if (n && (!u || !v || !out)) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        const double* du = dev_in(c, u, n, "cu");
+        const double* dv = dev_in(c, v, n, "cv");
+        DevOut<double> o(c, out, n, "cdf");
+        pcb::run_cdf(c, family, theta, du, dv, n, o.dev);
+        o.finish(c);
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int pcb_spearman_rho(pcb_context* ctx, int family, double theta, int quad_nodes, double* rho) {
+    return guarded(ctx, [&] {
+        check_family(family);
+        if (!theta_in_domain(family, theta)) throw pcb::Error(PCB_E_DOMAIN, "theta outside the family domain");
+        if (quad_nodes < 1 || quad_nodes > 65536) throw pcb::Error(PCB_E_INVALID, "spearman_rho: bad quad_nodes");
+        if (!rho) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        *rho = pcb::run_spearman(ctx->c, family, theta, quad_nodes);
+    });
+}
+
+int pcb_kendall_tau(pcb_context* ctx, const double* u1, const double* u2, uint64_t n_rows,
+                    const uint64_t* seg_offsets, uint64_t n_seg, uint64_t m_max, double* tau) {
+    return guarded(ctx, [&] {
+        pcb::Ctx& c = ctx->c;
+        const std::vector<uint64_t> off = check_offsets(seg_offsets, n_seg, n_rows, 0);
+        if (m_max < 2 || m_max > 8192) throw pcb::Error(PCB_E_INVALID, "kendall_tau: m_max must lie in [2, 8192]");
+        if (!u1 || !u2 || !tau) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
+        const double* d1 = dev_in(c, u1, n_rows, "k1");
+        const double* d2 = dev_in(c, u2, n_rows, "k2");
+        DevOut<double> o(c, tau, n_seg, "tau");
+        pcb::run_kendall(c, d1, d2, off, static_cast<uint32_t>(m_max), o.dev);
+        o.finish(c);
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+}  // extern "C"
+
+namespace {
+// quadrature.hpp:82-120: adaptive Simpson and the first Debye function
+template <class F>
+double simpson_step(F& f, double a, double b, double fa, double fm, double fb, double whole, double tol, int depth) {
+    const double m = 0.5 * (a + b), lm = 0.5 * (a + m), rm = 0.5 * (m + b);
+    const double flm = f(lm), frm = f(rm);
+    const double left = (m - a) / 6.0 * (fa + 4.0 * flm + fm), right = (b - m) / 6.0 * (fm + 4.0 * frm + fb);
+    const double delta = left + right - whole;
+    if (depth <= 0 || std::fabs(delta) <= 15.0 * tol) return left + right + delta / 15.0;
+    return simpson_step(f, a, m, fa, flm, fm, left, 0.5 * tol, depth - 1) +
+           simpson_step(f, m, b, fm, frm, fb, right, 0.5 * tol, depth - 1);
+}
+double debye1_host(double x) {
+    if (x == 0.0) return 1.0;
+    if (x < 0.0) return debye1_host(-x) - x / 2.0;
+    auto f = [](double t) { return t == 0.0 ? 1.0 : t / std::expm1(t); };
+    const double fa = f(0.0), fm = f(0.5 * x), fb = f(x);
+    return simpson_step(f, 0.0, x, fa, fm, fb, x / 6.0 * (fa + 4.0 * fm + fb), 1e-13 * std::max(1.0, x), 48) / x;
+}
+double model_tau(int fam, double t) {
+    if (fam == 0) return 2.0 / 3.14159265358979323846 * std::asin(t);
+    if (fam == 2) return 1.0 - 1.0 / t;
+    return 1.0 - 4.0 / t * (1.0 - debye1_host(t));
+}
+}  // namespace
+
+extern "C" {
+
+int pcb_model_kendall_tau(int family, double theta, double* tau) {
+    if (family < 0 || family > 2 || !tau) return PCB_E_INVALID;
+    if (!theta_in_domain(family, theta)) return PCB_E_DOMAIN;
+    *tau = model_tau(family, theta);
+    return PCB_OK;
+}
+
+int pcb_inverse_tau(int family, double tau, double* theta) {
+    if (family < 0 || family > 2 || !theta || !std::isfinite(tau)) return PCB_E_INVALID;
+    if (tau <= -1.0 || tau >= 1.0 || (family == 2 && tau < 0.0)) return PCB_E_DOMAIN;  // unattainable
+    if (family == 0) {
+        *theta = std::sin(0.5 * 3.14159265358979323846 * tau);
+    } else if (family == 2) {
+        *theta = 1.0 / (1.0 - tau);
+    } else {
+        if (tau == 0.0) return PCB_E_DOMAIN;  // the Frank family excludes theta = 0
+        const double at = std::fabs(tau);
+        double lo = 1e-9, hi = 1.0;
+        while (model_tau(1, hi) < at && hi < 1e6) hi *= 2.0;
+        for (int it = 0; it < 300 && hi - lo > 1e-12 * hi; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            (model_tau(1, mid) < at ? lo : hi) = mid;
+        }
+        *theta = tau < 0.0 ? -0.5 * (lo + hi) : 0.5 * (lo + hi);
+    }
+    return PCB_OK;
+}
+
 int pcb_measure_fp64_peak(pcb_context* ctx, double* v) {
     return guarded(ctx, [&] {
         if (!v) throw pcb::Error(PCB_E_INVALID, "NULL pointer");

@@ -183,6 +183,13 @@ void run_sample(Ctx& c, int family, double theta, uint64_t n_total, uint64_t k_t
 // sum (fa-fb)^2, sum fa, sum fa^2} (weighted)
 void run_rel_error(Ctx& c, int family, double ta, double tb, int nodes, double out4[4]);
 void gauss_legendre01(int n, std::vector<double>& x, std::vector<double>& w);
+// copula CDF (copula.hpp:273-290) per point; Spearman rho of the model by the
+// tensor rule; empirical Kendall tau of each segment's
+// first m_max rows (SPEC.md:243 init)
+void run_cdf(Ctx& c, int family, double theta, const double* u, const double* v, uint64_t n, double* out);
+double run_spearman(Ctx& c, int family, double theta, int nodes);
+void run_kendall(Ctx& c, const double* u1, const double* u2, const std::vector<uint64_t>& off, uint32_t m_max,
+                 double* tau);
 void run_strided_gather(Ctx& c, const double* src, uint64_t n_rows, uint64_t m, double* dst);
 
 double run_fp64_peak(Ctx& c);

@@ -90,6 +90,143 @@ __global__ void k_rel_total(const double* w, const double* rows, int n, double* 
     out[threadIdx.x] = t;
 }
 
+// ------------------------------------------------------- CDF and dependence
+// copula.hpp:273-290 cdf; normal.hpp:84-166 bvn_cdf (Drezner-Wesolowsky /
+// Genz with the 6/12/20-point Gauss-Legendre rules of bvn_rule).
+__constant__ double c_bvn_x[38], c_bvn_w[38];  // rules of 6, 12, 20 nodes on [-1, 1], concatenated
+
+__device__ __forceinline__ double dev_norm_cdf(double x) {  // normal.hpp:20-22
+    return 0.5 * erfc(-x * 0.70710678118654752440);
+}
+
+__device__ double bvn_upper_dev(double h, double k, double r) {  // normal.hpp:97-155
+    const double twopi = 6.283185307179586476925;
+    const double ar = fabs(r);
+    const int off = ar < 0.3 ? 0 : (ar < 0.75 ? 6 : 18), nn = ar < 0.3 ? 6 : (ar < 0.75 ? 12 : 20);
+    double hk = h * k, bvn = 0.0;
+    if (ar < 0.925) {
+        if (ar > 0.0) {
+            const double hs = 0.5 * (h * h + k * k), asr = asin(r);
+            for (int i = 0; i < nn; ++i) {
+                const double sn = sin(0.5 * asr * (c_bvn_x[off + i] + 1.0));
+                bvn += c_bvn_w[off + i] * exp((sn * hk - hs) / (1.0 - sn * sn));
+            }
+            bvn *= asr / (2.0 * twopi);
+        }
+        bvn += dev_norm_cdf(-h) * dev_norm_cdf(-k);
+    } else {
+        if (r < 0.0) {
+            k = -k;
+            hk = -hk;
+        }
+        if (ar < 1.0) {
+            const double as = (1.0 - r) * (1.0 + r);
+            double a = sqrt(as);
+            const double bs = (h - k) * (h - k), cc = (4.0 - hk) / 8.0, dd = (12.0 - hk) / 16.0;
+            double asr = -0.5 * (bs / as + hk);
+            if (asr > -100.0)
+                bvn = a * exp(asr) * (1.0 - cc * (bs - as) * (1.0 - dd * bs / 5.0) / 3.0 + cc * dd * as * as / 5.0);
+            if (-hk < 100.0) {
+                const double bb = sqrt(bs);
+                bvn -= exp(-0.5 * hk) * sqrt(twopi) * dev_norm_cdf(-bb / a) * bb *
+                       (1.0 - cc * bs * (1.0 - dd * bs / 5.0) / 3.0);
+            }
+            a *= 0.5;
+            for (int i = 0; i < nn; ++i) {
+                const double t = a * (c_bvn_x[off + i] + 1.0), xs = t * t;
+                asr = -0.5 * (bs / xs + hk);
+                if (asr > -100.0) {
+                    const double rs = sqrt(1.0 - xs);
+                    bvn += a * c_bvn_w[off + i] * exp(asr) *
+                           (exp(-hk * (1.0 - rs) / (2.0 * (1.0 + rs))) / rs - (1.0 + cc * xs * (1.0 + dd * xs)));
+                }
+            }
+            bvn = -bvn / twopi;
+        }
+        if (r > 0.0) {
+            bvn += dev_norm_cdf(-fmax(h, k));
+        } else {
+            bvn = -bvn;
+            if (k > h) bvn += dev_norm_cdf(k) - dev_norm_cdf(h);
+        }
+    }
+    return fmin(fmax(bvn, 0.0), 1.0);
+}
+
+__device__ __forceinline__ double frank_cdf_pos_dev(double u, double v, double t) {  // copula.hpp:174-181
+    const double lo = fmin(u, v), hi = fmax(u, v);
+    const double k2 = -t * (hi - lo);
+    const double b = expm1(-t * (1.0 - lo)) + exp(k2) * expm1(-t * lo);
+    return lo - (log(-b) - log(-expm1(-t))) / t;
+}
+
+__device__ double cdf_dev(int fam, double t, double u, double v) {  // copula.hpp:273-290 (u, v clamped)
+    if (fam == 0) return bvn_upper_dev(-dev_phi_inv(u), -dev_phi_inv(v), t);
+    if (fam == 1) return t > 0.0 ? frank_cdf_pos_dev(u, v, t) : u - frank_cdf_pos_dev(u, 1.0 - v, -t);
+    // Gumbel: exp(-W), W = S^{1/t} by exponent shifting (copula.hpp:199-213)
+    const double lx = log(-log(u)), ly = log(-log(v));
+    const double a = t * lx, b = t * ly, m = fmax(a, b);
+    const double lnS = m + log(exp(a - m) + exp(b - m));
+    return exp(-exp(lnS / t));
+}
+
+__global__ void k_cdf(int fam, double t, const double* u, const double* v, uint64_t n, double* out) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[i] = cdf_dev(fam, t, clamp_unit(u[i]), clamp_unit(v[i]));
+}
+
+// rows of the tensor rule for int C (Spearman rho = 12 int C - 3)
+__global__ void __launch_bounds__(256) k_cdf_rows(int fam, double t, const double* __restrict__ x,
+                                                 const double* __restrict__ w, int n, double* rows) {
+    const int i = blockIdx.x;
+    double v[1] = {0.0};
+    for (int j = threadIdx.x; j < n; j += blockDim.x) v[0] += w[j] * cdf_dev(fam, t, clamp_unit(x[i]), clamp_unit(x[j]));
+    __shared__ double sh[256 / 32];
+    block_sum<1>(v, sh);
+    if (threadIdx.x == 0) rows[i] = v[0];
+}
+
+__global__ void k_rows_total(const double* w, const double* rows, int n, double* out) {
+    if (threadIdx.x) return;
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += w[i] * rows[i];
+    *out = t;
+}
+
+// Empirical Kendall tau of each segment's first m rows, the oracle's
+// definition (sort by (u1, u2), strict inversions of u2): a pair counts when
+// u1 and u2 are strictly discordant. One CTA per segment, all pairs from
+// shared memory; integer counts, so the result is exact.
+__global__ void __launch_bounds__(1024) k_kendall(const double* u1, const double* u2, const uint64_t* off,
+                                                 uint32_t m_max, double* tau) {
+    extern __shared__ double kt[];
+    const uint64_t b = off[blockIdx.x];
+    const uint32_t m = static_cast<uint32_t>(min(static_cast<uint64_t>(m_max), off[blockIdx.x + 1] - b));
+    double* a1 = kt;
+    double* a2 = kt + m_max;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        a1[i] = u1[b + i];
+        a2[i] = u2[b + i];
+    }
+    __syncthreads();
+    unsigned long long sw = 0;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const double x = a1[i], y = a2[i];
+        uint32_t c = 0;
+        for (uint32_t j = i + 1; j < m; ++j) c += ((a1[j] < x) & (a2[j] > y)) | ((a1[j] > x) & (a2[j] < y));
+        sw += c;
+    }
+    __shared__ unsigned long long s_sw;
+    if (threadIdx.x == 0) s_sw = 0;
+    __syncthreads();
+    atomicAdd(&s_sw, sw);  // integer: order-independent
+    __syncthreads();
+    if (threadIdx.x == 0)
+        tau[blockIdx.x] = m < 2 ? 0.0 : 1.0 - 2.0 * static_cast<double>(s_sw) / (0.5 * static_cast<double>(m) *
+                                                                                  static_cast<double>(m - 1));
+}
+
 // ------------------------------------------------------------------ sampler
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {  // rng.hpp:15-20
     z += 0x9e3779b97f4a7c15ull;
@@ -208,9 +345,9 @@ void run_combine(Ctx& c, const void* d_records, uint64_t n, double* d_weights, d
     c.count_launch();
 }
 
-// n-point Gauss-Legendre rule on (0, 1) (quadrature.hpp:22-62): Newton on
-// P_n from cos(pi (i + 0.75) / (n + 0.5)), w = 2 / ((1 - x^2) P_n'(x)^2), mapped.
-void gauss_legendre01(int n, std::vector<double>& x, std::vector<double>& w) {
+// n-point Gauss-Legendre rule on [-1, 1] (quadrature.hpp:22-55): Newton on
+// P_n from cos(pi (i + 0.75) / (n + 0.5)), w = 2 / ((1 - x^2) P_n'(x)^2).
+void gauss_legendre_m11(int n, std::vector<double>& x, std::vector<double>& w) {
     x.assign(n, 0.0);
     w.assign(n, 0.0);
     const double pi = 3.14159265358979323846;
@@ -236,6 +373,11 @@ void gauss_legendre01(int n, std::vector<double>& x, std::vector<double>& w) {
         w[n - 1 - i] = wt;
     }
     if (n % 2 == 1) x[n / 2] = 0.0;
+}
+
+// the same rule mapped to (0, 1) (quadrature.hpp:58-64)
+void gauss_legendre01(int n, std::vector<double>& x, std::vector<double>& w) {
+    gauss_legendre_m11(n, x, w);
     for (int i = 0; i < n; ++i) {
         x[i] = 0.5 * (x[i] + 1.0);
         w[i] *= 0.5;
@@ -256,6 +398,60 @@ void run_rel_error(Ctx& c, int family, double ta, double tb, int nodes, double o
     c.count_launch(2);
     PCB_CUDA(cudaMemcpyAsync(out4, d_out, 4 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     PCB_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+void upload_bvn_rules() {
+    double hx[38], hw[38];
+    int o = 0;
+    for (int n : {6, 12, 20}) {
+        std::vector<double> x, w;
+        gauss_legendre_m11(n, x, w);
+        for (int i = 0; i < n; ++i) {
+            hx[o + i] = x[i];
+            hw[o + i] = w[i];
+        }
+        o += n;
+    }
+    PCB_CUDA(cudaMemcpyToSymbol(c_bvn_x, hx, sizeof hx));
+    PCB_CUDA(cudaMemcpyToSymbol(c_bvn_w, hw, sizeof hw));
+}
+
+void run_cdf(Ctx& c, int family, double theta, const double* u, const double* v, uint64_t n, double* out) {
+    upload_bvn_rules();
+    if (n == 0) return;
+    const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148u * 16u));
+    k_cdf<<<blocks, 256, 0, c.stream>>>(family, theta, u, v, n, out);
+    c.count_launch();
+}
+
+double run_spearman(Ctx& c, int family, double theta, int nodes) {
+    upload_bvn_rules();
+    std::vector<double> hx, hw;
+    gauss_legendre01(nodes, hx, hw);
+    auto* d_x = c.ws.get_t<double>("rho.x", nodes);
+    auto* d_w = c.ws.get_t<double>("rho.w", nodes);
+    auto* rows = c.ws.get_t<double>("rho.rows", nodes);
+    auto* d_out = c.ws.get_t<double>("rho.out", 1);
+    PCB_CUDA(cudaMemcpyAsync(d_x, hx.data(), nodes * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    PCB_CUDA(cudaMemcpyAsync(d_w, hw.data(), nodes * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    k_cdf_rows<<<nodes, 256, 0, c.stream>>>(family, theta, d_x, d_w, nodes, rows);
+    k_rows_total<<<1, 32, 0, c.stream>>>(d_w, rows, nodes, d_out);
+    c.count_launch(2);
+    double h = 0.0;
+    PCB_CUDA(cudaMemcpyAsync(&h, d_out, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    PCB_CUDA(cudaStreamSynchronize(c.stream));
+    return 12.0 * h - 3.0;
+}
+
+void run_kendall(Ctx& c, const double* u1, const double* u2, const std::vector<uint64_t>& off, uint32_t m_max,
+                 double* tau) {
+    const size_t K = off.size() - 1;
+    auto* d_off = c.ws.get_t<uint64_t>("kt.off", K + 1);
+    PCB_CUDA(cudaMemcpyAsync(d_off, off.data(), (K + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, c.stream));
+    const size_t smem = 2 * static_cast<size_t>(m_max) * sizeof(double);
+    PCB_CUDA(cudaFuncSetAttribute(k_kendall, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_kendall<<<static_cast<unsigned>(K), 1024, smem, c.stream>>>(u1, u2, d_off, m_max, tau);
+    c.count_launch();
 }
 
 void run_sample(Ctx& c, int family, double theta, uint64_t n_total, uint64_t k_total, uint64_t first, uint64_t last,
