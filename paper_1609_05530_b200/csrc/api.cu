@@ -171,6 +171,8 @@ void pipeline_blocks(pcb::Ctx& c, int fam, int prec, const double* d1, const dou
     io.rp = rb.r.rp;
     io.rank = &rb.r;
     io.bad = rb.bad;
+    io.x1 = d1;
+    io.x2 = d2;
     pcb::run_fit(c, io, d_out);
     finish_stage_times(c);
 }
@@ -373,6 +375,8 @@ int pcb_fit(pcb_context* ctx, int family, int precision, const double* u1, const
         io.off = off;
         io.u1 = d1;
         io.u2 = d2;
+        io.x1 = d1;
+        io.x2 = d2;
         io.rp = rb.r.rp;
         io.rank = &rb.r;
         DevOut<pcb_fit_result> o(c, out, n_seg, "fit");
@@ -412,6 +416,8 @@ int pcb_asymptotic_variance(pcb_context* ctx, int family, const double* theta_ha
         io.off = off;
         io.u1 = d1;
         io.u2 = d2;
+        io.x1 = d1;
+        io.x2 = d2;
         io.rp = rb.r.rp;
         io.rank = &rb.r;
         io.theta_in = dth;

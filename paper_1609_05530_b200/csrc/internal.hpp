@@ -141,6 +141,8 @@ struct FitIO {
     const double* u1 = nullptr;
     const double* u2 = nullptr;
     const int32_t* bad = nullptr;  // per segment, may be null
+    const double* x1 = nullptr;  // device columns the ranks came from (raw or pseudo-observations):
+    const double* x2 = nullptr;  // the PCB_INIT=tau start, rank-invariant
     const double* theta_in = nullptr;  // device: skip the fit, evaluate at these (variance API)
     bool do_fit = true;
     bool do_variance = true;

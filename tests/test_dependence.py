@@ -93,3 +93,20 @@ def test_device_empirical_kendall_equals_oracle(ctx, orc):
     # rank invariance: raw columns and their pseudo-observations agree
     U = pcb.normalized_ranks(pcb.DataMatrix(c1, c2), off, ctx=ctx)
     assert np.array_equal(pcb.empirical_kendall_tau(U.u1, U.u2, off, ctx=ctx), tau)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fam,theta", [(1, 5.0), (1, -3.0), (2, 2.0)])
+def test_tau_init_same_root(ctx, orc, monkeypatch, fam, theta):
+    """PCB_INIT=tau (the SPEC's start) reaches the same theta-hat as the default start."""
+    X = pcb.sample_matrix(fam, theta, 60000, 6, ctx=ctx)
+    off = [0, 10000, 20000, 30000, 40000, 50000, 60000]
+    a = pcb.fit_blocks(fam, X, off, ctx=ctx)
+    monkeypatch.setenv("PCB_INIT", "tau")
+    b = pcb.fit_blocks(fam, X, off, ctx=ctx)
+    want = orc.fit_blocks(fam, np.asarray(X.col1), np.asarray(X.col2), np.asarray(off, np.uint64))
+    for x, y, w in zip(a, b, want):
+        assert x.converged and y.converged
+        assert abs(y.theta_hat - w.theta_hat) <= 1e-9 * abs(w.theta_hat)
+        assert abs(y.sigma2 - w.sigma2) <= 1e-9 * abs(w.sigma2)
+        assert abs(x.theta_hat - y.theta_hat) <= 1e-9 * abs(w.theta_hat)
