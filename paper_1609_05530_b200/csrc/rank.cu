@@ -492,9 +492,8 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* recv_key = reinterpret_cast<unsigned long long*>(smem);
     uint32_t* outw = reinterpret_cast<uint32_t*>(recv_key + RCAP);  // the slot's result (after the sort)
-    uint32_t* lhw = outw;                                   // during the sort: NBL u16 counts -> cursors
-    uint16_t* lbs = reinterpret_cast<uint16_t*>(lhw + NBL / 2);  // during the sort: local bucket per slot
-    uint16_t* lhs = reinterpret_cast<uint16_t*>(outw + RCAP);    // NBL+1 u16 starts (+1 pad)
+    uint16_t* lhs = reinterpret_cast<uint16_t*>(outw + RCAP);    // NBL u16 counts -> NBL+1 starts (+1 pad)
+    uint32_t* lhw = reinterpret_cast<uint32_t*>(lhs);             // the counts, two per word
     uint16_t* perm = lhs + NBL + 2;
 
     // the slice is staged into the (not yet used) receive buffer by one bulk
@@ -758,19 +757,20 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     // recomputed from the key)
     const uint32_t T = s_total, base = s_base;
     const uint32_t lmask = NBL - 1u;
-    for (uint32_t q = tid; q < NBL / 2; q += CT) lhw[q] = 0u;
+    for (uint32_t q = tid; q <= NBL / 2; q += CT) lhw[q] = 0u;
     __syncthreads();
+    // the counting atomic's old value is the element's index inside its bucket:
+    // outw[j] = bucket | index << 14 (NBL <= 16384), so the placement needs no second atomic
     for (uint32_t j = tid; j < T; j += CT) {
-        const uint32_t lb = cbucket(recv_key[j], hm, scale, nbtot) & lmask;
-        lbs[j] = static_cast<uint16_t>(lb);
-        atomicAdd(lhw + (lb >> 1), 1u << ((lb & 1) * 16));
+        const uint32_t lb = cbucket(recv_key[j], hm, scale, nbtot) & lmask, sh = (lb & 1) * 16;
+        const uint32_t idx = (atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu;
+        outw[j] = lb | (idx << 14);
     }
     __syncthreads();
-    block_scan_excl_u16(lhw, lhs, NBL, s_w);  // counts < 2^16: a bucket never exceeds RCAP < 65535
+    block_scan_excl_u16(lhw, lhs, NBL, s_w);  // in place: counts -> starts (bucket sizes < 2^16)
     for (uint32_t j = tid; j < T; j += CT) {
-        const uint32_t lb = lbs[j], sh = (lb & 1) * 16;
-        const uint32_t slot = (atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu;
-        perm[slot] = static_cast<uint16_t>(j);
+        const uint32_t w = outw[j];
+        perm[lhs[w & 0x3fffu] + (w >> 14)] = static_cast<uint16_t>(j);
     }
     __syncthreads();
 
@@ -781,14 +781,14 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     //   outw = (local r2 << 16) | local sorted position | run-start bit
     // walk the elements in bucket order: a warp's lanes mostly share buckets, so
     // the bucket-mate loads are shared-memory broadcasts
-    uint32_t keep[QMAX];  // results stay in registers while lbs (aliased by outw) is still read
+    uint32_t keep[QMAX];  // results stay in registers while outw still holds the buckets
 #pragma unroll
     for (int k = 0; k < QMAX; ++k) {
         const uint32_t qq = tid + k * CT;
         if (qq >= T) break;
         const uint32_t j = perm[qq];
         const unsigned long long kv = recv_key[j];
-        const uint32_t lb = lbs[j];
+        const uint32_t lb = outw[j] & 0x3fffu;
         const uint32_t s0 = lhs[lb], s1 = lhs[lb + 1];
         uint32_t less = 0, same = 0, before = 0;
 #pragma unroll 1
