@@ -14,6 +14,19 @@
 
 namespace pcb {
 
+// 1/x for the per-point paths: MUFU reciprocal + two Newton steps (about one
+// ulp; the 1e-9 parity bar is far away), no IEEE-division slow path. Inputs
+// are normal positive or negative doubles (never 0, inf or denormal here).
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+
 // ------------------------------------------------------------------ normal
 __device__ __forceinline__ double dev_phi_pdf(double x) {  // normal.hpp:15-18
     return 0.3989422804014326779399 * exp(-0.5 * x * x);
@@ -175,7 +188,7 @@ __device__ __forceinline__ void frank_sh(double u, double v, const FrankTheta& f
     const double sum = lo + hi;
     const double bp = lo - e1 + e2 * (hi - sum * e3);
     const double bpp = e1 - lo * lo + e2 * (sum * sum * e3 - hi * hi);
-    const double rb = 1.0 / b;
+    const double rb = fast_rcp(b);
     const double q = bp * rb;
     const double sc = f.inv_t - f.g - sum - 2.0 * q;
     s = f.neg ? -sc : sc;
@@ -250,7 +263,7 @@ __device__ __forceinline__ PointFull frank_full(double u, double v, const FrankT
     const double sum = lo + hi;
     const double bp = lo - e1 + e2 * (hi - sum * e3);
     const double bpp = e1 - lo * lo + e2 * (sum * sum * e3 - hi * hi);
-    const double rb = 1.0 / b;
+    const double rb = fast_rcp(b);
     const double q = bp * rb;
     PointFull p;
     p.logc = f.logc_const + k2 - 2.0 * log(-b);
@@ -295,7 +308,7 @@ __device__ __forceinline__ void gumbel_sh(double lx, double ly, const GumbelThet
     const double lmax = amax ? lx : ly, lmin = amax ? ly : lx;
     const double e = exp((amax ? b : a) - m);  // the other exponential is exactly 1 (copula.hpp:209-210)
     const double sden = 1.0 + e;
-    const double rs = 1.0 / sden;
+    const double rs = fast_rcp(sden);
     const double lnS = m + log(sden);
     const double w = exp(lnS * g.inv_t);
     const double r = (lmax + e * lmin) * rs;
@@ -306,7 +319,7 @@ __device__ __forceinline__ void gumbel_sh(double lx, double ly, const GumbelThet
     const double lw_tt = rt * g.inv_t - 2.0 * r * g.inv_t2 + 2.0 * lnS * g.inv_t3;
     const double wtt = w * (lw_t * lw_t + lw_tt);
     const double gg = w + g.t - 1.0;
-    const double rg = 1.0 / gg;
+    const double rg = fast_rcp(gg);
     const double wt1 = wt + 1.0;
     s = -wt + lx + ly - lnS * g.inv_t2 + g.c1t * r + wt1 * rg;
     h = -wtt - 2.0 * r * g.inv_t2 + 2.0 * lnS * g.inv_t3 + g.c1t * rt + (wtt * gg - wt1 * wt1) * rg * rg;
@@ -362,7 +375,7 @@ __device__ __forceinline__ PointFull gumbel_full_t(double lx, double ly, double 
     const double e = exp((amax ? b : a) - m);
     const double ea = amax ? 1.0 : e, eb = amax ? e : 1.0;
     const double sden = 1.0 + e;
-    const double rs = 1.0 / sden;
+    const double rs = fast_rcp(sden);
     const double lnS = m + log(sden);
     const double w = exp(lnS * g.inv_t);
     const double r = (ea * lx + eb * ly) * rs;
@@ -374,7 +387,7 @@ __device__ __forceinline__ PointFull gumbel_full_t(double lx, double ly, double 
     const double lw_tt = rt * g.inv_t - 2.0 * r * g.inv_t2 + 2.0 * lnS * g.inv_t3;
     const double wtt = w * (lw_t * lw_t + lw_tt);
     const double gg = w + g.t - 1.0;
-    const double rg = 1.0 / gg;
+    const double rg = fast_rcp(gg);
     const double wt1 = wt + 1.0;
     PointFull p;
     p.logc = -w + (g.t - 1.0) * (lx + ly) + (x + y) + g.c1t * lnS + log(gg);
@@ -399,13 +412,13 @@ __device__ __forceinline__ PointFull gumbel_full_t(double lx, double ly, double 
 
 __device__ __forceinline__ PointFull gumbel_full(double u, double v, const GumbelTheta& g) {
     const double x = -log(u), y = -log(v);
-    return gumbel_full_t(log(x), log(y), x, y, 1.0 / x, 1.0 / y, 1.0 / u, 1.0 / v, g);
+    return gumbel_full_t(log(x), log(y), x, y, fast_rcp(x), fast_rcp(y), fast_rcp(u), fast_rcp(v), g);
 }
 
 // from the hoisted (ln x, ln y) pair of the prepare pass
 __device__ __forceinline__ PointFull gumbel_full_l(double u, double v, double lx, double ly, const GumbelTheta& g) {
     const double x = exp(lx), y = exp(ly);
-    return gumbel_full_t(lx, ly, x, y, 1.0 / x, 1.0 / y, 1.0 / u, 1.0 / v, g);
+    return gumbel_full_t(lx, ly, x, y, fast_rcp(x), fast_rcp(y), fast_rcp(u), fast_rcp(v), g);
 }
 
 // log c only (pseudo_loglik API), any family; u, v already clamped.
