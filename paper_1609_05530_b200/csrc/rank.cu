@@ -379,6 +379,7 @@ struct ClusterPlan {
     uint32_t rcap = 0;     // receive capacity per CTA
     uint32_t lg_nbl = 0;   // log2 local buckets per CTA
     size_t smem = 0;
+    bool lean = false;     // 512-thread CTAs, two per SM (k_rank_cluster_t<512, true>)
 };
 
 inline bool getenv_flag(const char* name) {
@@ -390,9 +391,10 @@ __host__ __device__ inline uint32_t slice_of(uint64_t n, int cl) {
     return static_cast<uint32_t>(((n + cl - 1) / cl + 31) & ~31ull);
 }
 
-inline ClusterPlan plan_for(uint64_t nmax, int cl) {
+inline ClusterPlan plan_for(uint64_t nmax, int cl, bool lean = false) {
     ClusterPlan p;
     p.cl = cl;
+    p.lean = lean;
     p.s = slice_of(nmax, cl);
     const uint32_t slack = std::max<uint32_t>(256u, static_cast<uint32_t>(5.5 * std::sqrt(static_cast<double>(p.s))));
     p.rcap = (p.s + slack + 31u) & ~31u;
@@ -402,13 +404,27 @@ inline ClusterPlan plan_for(uint64_t nmax, int cl) {
     // per slot: key 8 + result 4 (aliased by the NBL u16 counters and the
     // slot's u16 local bucket during the local sort; NBL <= S < RCAP) + perm 2;
     // NBL+2 u16 bucket starts
-    p.smem = static_cast<size_t>(p.rcap) * 14 + (static_cast<size_t>(1u << lg) + 2) * 2 + 64;
+    p.smem = static_cast<size_t>(p.rcap) * (lean ? 10 : 14) + (static_cast<size_t>(1u << lg) + 2) * 2 + 64;
     return p;
 }
+
+constexpr int kLeanT = 512;   // threads of a lean CTA
+constexpr int kLeanQ = 18;    // received elements per lean thread
+constexpr size_t kLeanSmem = 112 * 1024 - 4096;  // two per SM beside their static shared memory
 
 inline ClusterPlan plan_cluster(uint64_t nmax) {
     int forced = 0;
     if (const char* v = std::getenv("PCB_RANK_CL")) forced = std::atoi(v);
+    // lean (two CTAs per SM, opt-in with PCB_RANK_LEAN=1): measured slower at
+    // C5 (16-CTA clusters, 42.7 vs 38.2 ms per family) — kept as a variant
+    if (getenv_flag("PCB_RANK_LEAN"))
+        for (int cl = 2; cl <= kMaxCluster; ++cl) {
+            if (forced && cl != forced) continue;
+            ClusterPlan p = plan_for(nmax, cl, true);
+            if (p.rcap <= static_cast<uint32_t>(kLeanQ * kLeanT) && p.smem <= kLeanSmem &&
+                p.s <= static_cast<uint32_t>(EMAX * kLeanT))
+                return p;
+        }
     for (int cl = 1; cl <= kMaxCluster; ++cl) {
         if (forced && cl != forced) continue;
         ClusterPlan p = plan_for(nmax, cl);
@@ -426,10 +442,11 @@ __device__ __forceinline__ uint32_t cbucket(unsigned long long k, double hm, dou
 
 // Same scan over NBL u16 counters packed two per word (`cw`); writes the u16
 // starts (start[n] = total) and turns cw into cursors (packed starts).
+template <int CTT>
 __device__ void block_scan_excl_u16(uint32_t* cw, uint16_t* start, uint32_t n, uint32_t* s_w) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint32_t nw = n / 2;
-    const uint32_t per = (nw + CT - 1) / CT;
+    const uint32_t per = (nw + CTT - 1) / CTT;
     const uint32_t b0 = min(nw, tid * per), b1 = min(nw, b0 + per);
     uint32_t loc = 0;
     for (uint32_t q = b0; q < b1; ++q) loc += (cw[q] & 0xffffu) + (cw[q] >> 16);
@@ -442,13 +459,13 @@ __device__ void block_scan_excl_u16(uint32_t* cw, uint16_t* start, uint32_t n, u
     if (lane == 31) s_w[wid] = x;
     __syncthreads();
     if (wid == 0) {
-        uint32_t z = lane < NWARP ? s_w[lane] : 0u;
+        uint32_t z = lane < (CTT / 32) ? s_w[lane] : 0u;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
             if (lane >= o) z += y;
         }
-        if (lane < NWARP) s_w[lane] = z;
+        if (lane < (CTT / 32)) s_w[lane] = z;
     }
     __syncthreads();
     uint32_t run = (wid ? s_w[wid - 1] : 0u) + x - loc;
@@ -460,17 +477,23 @@ __device__ void block_scan_excl_u16(uint32_t* cw, uint16_t* start, uint32_t n, u
         cw[q] = s0 | (s1 << 16);
         run = s1 + (w >> 16);
     }
-    if (tid == CT - 1) start[n] = static_cast<uint16_t>(run);
+    if (tid == CTT - 1) start[n] = static_cast<uint16_t>(run);
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, const double* c0, const double* c1,
+// CTT threads per CTA. LEAN (512 threads, 2 CTAs per SM): no per-slot result
+// array — the local sort keeps (bucket, index) in registers and the ranking
+// recomputes the bucket from the key; results are staged in the receive
+// buffer once the ranking is done — so a CTA needs 10 B per slot.
+template <int CTT, bool LEAN>
+__global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const ClusterJob* jobs, const double* c0, const double* c1,
                                                        uint64_t n_rows, unsigned long long* rp, uint32_t* route,
                                                        uint32_t* r2s_g, uint16_t* posl_g, uint32_t* ocnt, uint32_t K,
                                                        int32_t* fb,
                                                        int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
                                                        int tail, unsigned long long* prof) {
     namespace cg = cooperative_groups;
+    constexpr int QM = LEAN ? 18 : QMAX;  // received elements per thread (RCAP <= QM * CTT)
     long long t_prev = clock64();
     auto mark = [&](int k) {  // optional phase timing (PCB_RANK_PROFILE): thread 0's clock deltas
         if (prof && threadIdx.x == 0) {
@@ -491,8 +514,10 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
 
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* recv_key = reinterpret_cast<unsigned long long*>(smem);
-    uint32_t* outw = reinterpret_cast<uint32_t*>(recv_key + RCAP);  // the slot's result (after the sort)
-    uint16_t* lhs = reinterpret_cast<uint16_t*>(outw + RCAP);    // NBL u16 counts -> NBL+1 starts (+1 pad)
+    // LEAN: results staged in the receive buffer after the ranking
+    uint32_t* outw = LEAN ? reinterpret_cast<uint32_t*>(recv_key) : reinterpret_cast<uint32_t*>(recv_key + RCAP);
+    uint16_t* lhs = LEAN ? reinterpret_cast<uint16_t*>(recv_key + RCAP)
+                         : reinterpret_cast<uint16_t*>(outw + RCAP);  // NBL u16 counts -> NBL+1 starts (+1 pad)
     uint32_t* lhw = reinterpret_cast<uint32_t*>(lhs);             // the counts, two per word
     uint16_t* perm = lhs + NBL + 2;
 
@@ -530,14 +555,14 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
             : "memory");
     };
 
-    __shared__ unsigned long long s_k[2][NWARP];
+    __shared__ unsigned long long s_k[2][(CTT / 32)];
     __shared__ unsigned long long s_rmin, s_rmax, s_gmin, s_gmax;  // s_rmin/s_rmax are read by peers
     __shared__ int s_bad, s_gbad, s_over;
-    __shared__ uint32_t s_wc[NWARP][kMaxCluster];  // per-warp counts -> per-warp send cursors
+    __shared__ uint32_t s_wc[(CTT / 32)][kMaxCluster];  // per-warp counts -> per-warp send cursors
     __shared__ uint32_t s_cnt[kMaxCluster];         // this CTA's sends per owner (read by peers)
     __shared__ uint32_t s_mat[kMaxCluster * kMaxCluster];
     __shared__ uint32_t s_off[kMaxCluster], s_total, s_base;
-    __shared__ uint32_t s_w[NWARP];
+    __shared__ uint32_t s_w[(CTT / 32)];
 
     // ---- 1. bucket-map range from a strided sample (one element per thread).
     // Any monotone map gives exact ranks (values outside the sampled range
@@ -546,7 +571,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     unsigned long long kmn = ~0ull, kmx = 0ull;
     const uint32_t len = e - a;
     if (len > 0) {
-        const unsigned long long kk = order_key(x[a + static_cast<uint32_t>((static_cast<uint64_t>(tid) * len) / CT)]);
+        const unsigned long long kk = order_key(x[a + static_cast<uint32_t>((static_cast<uint64_t>(tid) * len) / CTT)]);
         kmn = kk;
         kmx = kk;
     }
@@ -595,7 +620,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
         __syncthreads();
     };
     if (tid == 0) s_bad = 0;
-    for (int q = tid; q < NWARP * kMaxCluster; q += CT) (&s_wc[0][0])[q] = 0u;
+    for (int q = tid; q < (CTT / 32) * kMaxCluster; q += CTT) (&s_wc[0][0])[q] = 0u;
     cta_extremes();
     cluster.sync();
     mark(0);
@@ -603,7 +628,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     if (s_gmin == s_gmax) {  // exact extremes over every element (all CTAs agree on taking this branch)
         kmn = ~0ull;
         kmx = 0ull;
-        for (uint32_t i = a + tid; i < e; i += CT) {
+        for (uint32_t i = a + tid; i < e; i += CTT) {
             const unsigned long long kk = order_key(x[i]);
             kmn = min(kmn, kk);
             kmx = max(kmx, kk);
@@ -627,7 +652,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
                 fb[jid] = 2;  // handled, no route
             }
         } else if (constant) {  // one tie run: avg rank (n+1)/2 for all, stable positions = row order
-            for (uint32_t i = a + tid; i < e; i += CT)
+            for (uint32_t i = a + tid; i < e; i += CTT)
                 rp[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = pack_rank(J.n + 1u, i, i == 0);
             if (r == 0 && tid == 0) fb[jid] = 2;  // ranked, no route
         } else if (r == 0 && tid == 0) {
@@ -646,7 +671,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     wait_slice();  // the mbarrier was initialised before the first __syncthreads
 #pragma unroll
     for (int k = 0; k < EMAX; ++k) {
-        const uint32_t i = a + k * CT + tid;
+        const uint32_t i = a + k * CTT + tid;
         if (i < e) {
             const double v = xs[i];
             fin &= isfinite(v);
@@ -658,7 +683,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     if (!__syncthreads_and(fin) && tid == 0) s_bad = 1;  // validate_data (pseudo_obs.hpp:34-36)
     if (tid < CL) {  // totals per owner, and per-warp exclusive bases
         uint32_t run = 0;
-        for (int w = 0; w < NWARP; ++w) {
+        for (int w = 0; w < (CTT / 32); ++w) {
             const uint32_t c = s_wc[w][tid];
             s_wc[w][tid] = run;
             run += c;
@@ -708,7 +733,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
         mark(2);
         return;
     }
-    for (int q = tid; q < NWARP * CL; q += CT) s_wc[q / CL][q % CL] += s_off[q % CL];
+    for (int q = tid; q < (CTT / 32) * CL; q += CTT) s_wc[q / CL][q % CL] += s_off[q % CL];
     __syncthreads();
 
     // ---- 3. scatter keys to the owners (one 8-byte DSMEM store per element).
@@ -718,7 +743,7 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     if (tail) {
 #pragma unroll
       for (int k = 0; k < EMAX; ++k) {
-        const uint32_t i = a + k * CT + tid;
+        const uint32_t i = a + k * CTT + tid;
         if (i < e) {
             const unsigned long long kk = order_key(xs[i]);
             const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
@@ -730,17 +755,17 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     } else
 #pragma unroll
     for (int h = 0; h < EMAX; h += SB) {
-      if (a + h * CT >= e) break;
+      if (a + h * CTT >= e) break;
       double xv[SB];
 #pragma unroll
       for (int k = 0; k < SB; ++k) {
-        const uint32_t i = a + (h + k) * CT + tid;
+        const uint32_t i = a + (h + k) * CTT + tid;
         xv[k] = i < e ? x[i] : 0.0;
       }
 #pragma unroll
       for (int kk2 = 0; kk2 < SB; ++kk2) {
         const int k = h + kk2;
-        const uint32_t i = a + k * CT + tid;
+        const uint32_t i = a + k * CTT + tid;
         if (i < e) {
             const unsigned long long kk = order_key(xv[kk2]);
             const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
@@ -757,20 +782,39 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     // recomputed from the key)
     const uint32_t T = s_total, base = s_base;
     const uint32_t lmask = NBL - 1u;
-    for (uint32_t q = tid; q <= NBL / 2; q += CT) lhw[q] = 0u;
+    for (uint32_t q = tid; q <= NBL / 2; q += CTT) lhw[q] = 0u;
     __syncthreads();
     // the counting atomic's old value is the element's index inside its bucket:
     // outw[j] = bucket | index << 14 (NBL <= 16384), so the placement needs no second atomic
-    for (uint32_t j = tid; j < T; j += CT) {
-        const uint32_t lb = cbucket(recv_key[j], hm, scale, nbtot) & lmask, sh = (lb & 1) * 16;
-        const uint32_t idx = (atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu;
-        outw[j] = lb | (idx << 14);
-    }
-    __syncthreads();
-    block_scan_excl_u16(lhw, lhs, NBL, s_w);  // in place: counts -> starts (bucket sizes < 2^16)
-    for (uint32_t j = tid; j < T; j += CT) {
-        const uint32_t w = outw[j];
-        perm[lhs[w & 0x3fffu] + (w >> 14)] = static_cast<uint16_t>(j);
+    uint32_t keep[QM];  // LEAN: (bucket | index) of slot tid + k*CTT, then the ranking's results
+    if constexpr (LEAN) {
+#pragma unroll
+        for (int k2 = 0; k2 < QM; ++k2) {
+            const uint32_t j = tid + k2 * CTT;
+            if (j >= T) break;
+            const uint32_t lb = cbucket(recv_key[j], hm, scale, nbtot) & lmask, sh = (lb & 1) * 16;
+            keep[k2] = lb | (((atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu) << 14);
+        }
+        __syncthreads();
+        block_scan_excl_u16<CTT>(lhw, lhs, NBL, s_w);
+#pragma unroll
+        for (int k2 = 0; k2 < QM; ++k2) {
+            const uint32_t j = tid + k2 * CTT;
+            if (j >= T) break;
+            perm[lhs[keep[k2] & 0x3fffu] + (keep[k2] >> 14)] = static_cast<uint16_t>(j);
+        }
+    } else {
+        for (uint32_t j = tid; j < T; j += CTT) {
+            const uint32_t lb = cbucket(recv_key[j], hm, scale, nbtot) & lmask, sh = (lb & 1) * 16;
+            const uint32_t idx = (atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu;
+            outw[j] = lb | (idx << 14);
+        }
+        __syncthreads();
+        block_scan_excl_u16<CTT>(lhw, lhs, NBL, s_w);  // in place: counts -> starts (bucket sizes < 2^16)
+        for (uint32_t j = tid; j < T; j += CTT) {
+            const uint32_t w = outw[j];
+            perm[lhs[w & 0x3fffu] + (w >> 14)] = static_cast<uint16_t>(j);
+        }
     }
     __syncthreads();
 
@@ -781,14 +825,13 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     //   outw = (local r2 << 16) | local sorted position | run-start bit
     // walk the elements in bucket order: a warp's lanes mostly share buckets, so
     // the bucket-mate loads are shared-memory broadcasts
-    uint32_t keep[QMAX];  // results stay in registers while outw still holds the buckets
 #pragma unroll
-    for (int k = 0; k < QMAX; ++k) {
-        const uint32_t qq = tid + k * CT;
+    for (int k = 0; k < QM; ++k) {
+        const uint32_t qq = tid + k * CTT;
         if (qq >= T) break;
         const uint32_t j = perm[qq];
         const unsigned long long kv = recv_key[j];
-        const uint32_t lb = outw[j] & 0x3fffu;
+        const uint32_t lb = LEAN ? (cbucket(kv, hm, scale, nbtot) & lmask) : (outw[j] & 0x3fffu);
         const uint32_t s0 = lhs[lb], s1 = lhs[lb + 1];
         uint32_t less = 0, same = 0, before = 0;
 #pragma unroll 1
@@ -805,15 +848,15 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < QMAX; ++k) {
-        const uint32_t qq = tid + k * CT;
+    for (int k = 0; k < QM; ++k) {
+        const uint32_t qq = tid + k * CTT;
         if (qq >= T) break;
         outw[perm[qq]] = keep[k];
     }
     __syncthreads();
     const uint64_t reg = ((static_cast<uint64_t>(J.col) * K + J.seg) * CL + r) * RCAP;
     if (tid == 0) ocnt[(static_cast<uint64_t>(J.col) * K + J.seg) * CL + r] = T;
-    for (uint32_t j = tid; j < T; j += CT) {  // coalesced, in slot order
+    for (uint32_t j = tid; j < T; j += CTT) {  // coalesced, in slot order
         const uint32_t w = outw[j];
         r2s_g[reg + j] = 2u * base + (w >> 16);
         posl_g[reg + j] = static_cast<uint16_t>(w & 0xffffu);
@@ -823,21 +866,21 @@ __global__ void __launch_bounds__(CT, 1) k_rank_cluster(const ClusterJob* jobs, 
 
 void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, uint32_t njobs, const double* c0,
                          const double* c1, uint64_t n_rows, RankOut& out, int32_t* fb, int32_t* bad) {
-    // tail mode when the slice fits after the receive buffer
+    auto kern = p.lean ? k_rank_cluster_t<kLeanT, true> : k_rank_cluster_t<CT, false>;
+    // tail mode when the slice fits after the receive buffer (full CTAs only)
     cudaFuncAttributes fa;
-    PCB_CUDA(cudaFuncGetAttributes(&fa, k_rank_cluster));
+    PCB_CUDA(cudaFuncGetAttributes(&fa, kern));
     int optin = 0;
     PCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
     const size_t tail_bytes = static_cast<size_t>(p.rcap) * 8 + (static_cast<size_t>(p.s) + 2) * 8 + 16;
-    const int tail = (tail_bytes + fa.sharedSizeBytes <= static_cast<size_t>(optin) && !getenv_flag("PCB_RANK_NO_TAIL"))
-                         ? 1 : 0;
+    const int tail = (!p.lean && tail_bytes + fa.sharedSizeBytes <= static_cast<size_t>(optin) &&
+                      !getenv_flag("PCB_RANK_NO_TAIL")) ? 1 : 0;
     const size_t smem = tail ? std::max(p.smem, tail_bytes) : p.smem;
-    PCB_CUDA(cudaFuncSetAttribute(k_rank_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-    if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(k_rank_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    PCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(njobs * static_cast<uint32_t>(p.cl));
-    cfg.blockDim = dim3(CT);
+    cfg.blockDim = dim3(p.lean ? kLeanT : CT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
@@ -852,7 +895,7 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
         prof = c.ws.get_t<unsigned long long>("rank.prof", 8);
         PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
     }
-    PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_cluster, jobs, c0, c1, n_rows, out.rp, out.route, out.r2s, out.posl,
+    PCB_CUDA(cudaLaunchKernelEx(&cfg, kern, jobs, c0, c1, n_rows, out.rp, out.route, out.r2s, out.posl,
                                 out.ocnt,
                                 njobs / 2, fb, bad, p.cl, p.rcap, p.lg_nbl, tail, prof));
     if (prof) {
@@ -860,8 +903,8 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
         PCB_CUDA(cudaStreamSynchronize(c.stream));
         const double ctas = static_cast<double>(njobs) * p.cl;
-        std::fprintf(stderr, "[rank profile] CL=%d S=%u: cycles/CTA  minmax %.0f  count %.0f  matrix %.0f  send %.0f  "
-                     "localsort %.0f  rank %.0f\n", p.cl, p.s, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
+        std::fprintf(stderr, "[rank profile] CL=%d S=%u lean=%d: cycles/CTA  minmax %.0f  count %.0f  matrix %.0f  "
+                     "send %.0f  localsort %.0f  rank %.0f\n", p.cl, p.s, int(p.lean), h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
                      h[4] / ctas, h[5] / ctas);
     }
     c.count_launch();

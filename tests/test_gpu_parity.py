@@ -303,6 +303,23 @@ def test_rank_forced_global_path_identical(ctx, env):
     assert np.array_equal(a.u1, b.u1) and np.array_equal(a.u2, b.u2)
 
 
+def test_rank_lean_variant_identical(ctx, orc, env):
+    """The opt-in two-CTAs-per-SM rank kernel (PCB_RANK_LEAN=1) ranks bit-identically and feeds the same fit."""
+    rng = np.random.default_rng(11)
+    n = 250000
+    X = pcb.DataMatrix(rng.uniform(size=n), np.round(rng.standard_normal(n), 3))
+    off = np.linspace(0, n, 3).astype(np.uint64)
+    a = pcb.normalized_ranks(X, off, ctx=ctx)
+    env.setenv("PCB_RANK_LEAN", "1")
+    b = pcb.normalized_ranks(X, off, ctx=ctx)
+    assert np.array_equal(a.u1, b.u1) and np.array_equal(a.u2, b.u2)
+    assert np.array_equal(b.u2, oracle_ranks(orc, X.col2, off))
+    Y = pcb.sample_matrix(2, 2.0, 125000, 1, ctx=ctx)
+    r = pcb.fit_blocks(2, Y, [0, 125000], ctx=ctx)[0]
+    w = orc.fit_blocks(2, np.asarray(Y.col1), np.asarray(Y.col2), np.array([0, 125000], np.uint64))[0]
+    assert abs(r.theta_hat - w.theta_hat) <= 1e-9 * w.theta_hat and abs(r.sigma2 - w.sigma2) <= 1e-9 * w.sigma2
+
+
 @pytest.mark.parametrize("fam,theta", FAMS)
 def test_variance_cluster_vs_global(ctx, orc, env, fam, theta):
     n, k = 60000, 3
