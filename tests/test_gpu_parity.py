@@ -356,3 +356,54 @@ def test_host_streaming_identical(ctx, env):
     assert [(r.theta_hat, r.sigma2, r.loglik) for r in host] == [(r.theta_hat, r.sigma2, r.loglik) for r in devr]
     res = pcb.fit_parallel(2, X, k, ctx=ctx)
     assert res.theta_combined == pcb.combine(devr, ctx=ctx).theta_combined
+
+
+# --------------------------------------------------- BASELINE configs as parity cases
+def test_config_c2_full_parity(ctx, orc):
+    """configs[1] (C2): Frank theta=5, n=1e6, K=100 subsets of 1e4 — every block against the oracle."""
+    n, k = 1_000_000, 100
+    X = pcb.sample_matrix(1, 5.0, n, k, ctx=ctx)
+    res = pcb.fit_parallel(1, X, k, ctx=ctx)
+    off = orc.partition(n, k)
+    want = orc.fit_blocks(1, X.col1, X.col2, off)
+    check_records(res.per_block, want, TOL64)
+    tc, w, used = orc.combine(want)
+    assert res.blocks_used == used == k and rel(res.theta_combined, tc) <= TOL64
+    assert abs(res.theta_combined - 5.0) < 0.05
+
+
+def test_config_c3_sampled_parity_and_invariants(ctx, orc):
+    """configs[2] (C3): Gumbel theta=2, n=1e8, K=1000 subsets of 1e5 on device; eight blocks against the
+    oracle on the same bytes, SPEC.md:304-308 invariants over all of them."""
+    import torch
+    n, k = 100_000_000, 1000
+    X = pcb.sample_matrix(2, 2.0, n, k, device_out=True, ctx=ctx)
+    res = pcb.fit_parallel(2, X, k, ctx=ctx)
+    assert res.blocks_used == k and all(r.converged for r in res.per_block)
+    q = n // k
+    for m in (0, 1, 137, 500, 501, 777, 998, 999):
+        c1 = X.col1[m * q:(m + 1) * q].cpu().numpy()
+        c2 = X.col2[m * q:(m + 1) * q].cpu().numpy()
+        w = orc.fit_blocks(2, c1, c2, np.array([0, q], np.uint64))[0]
+        check_records([res.per_block[m]], [w], TOL64)
+    th = np.array([r.theta_hat for r in res.per_block])
+    assert th.min() <= res.theta_combined <= th.max()  # convexity
+    assert abs(res.theta_combined - 2.0) < 0.01
+    scaled = [pcb.FitResult(r.theta_hat, 3.0 * r.sigma2, r.n, r.loglik, r.iterations, r.converged)
+              for r in res.per_block]
+    assert rel(pcb.combine(scaled, ctx=ctx).theta_combined, res.theta_combined) <= 1e-13  # weight-scale invariance
+    del X
+    torch.cuda.empty_cache()
+
+
+EXTREME = [(0, 0.99), (0, -0.99), (0, 0.0), (1, 35.0), (1, -30.0), (1, 0.05), (2, 1.0), (2, 15.0)]
+
+
+@pytest.mark.parametrize("fam,theta", EXTREME)
+def test_fit_extreme_parameters(ctx, orc, fam, theta):
+    n, k = 30000, 3
+    X = pcb.sample_matrix(fam, theta, n, k, ctx=ctx)
+    off = orc.partition(n, k)
+    got = pcb.fit_blocks(fam, X, off, ctx=ctx)
+    want = orc.fit_blocks(fam, X.col1, X.col2, off)
+    check_records(got, want, TOL64)
