@@ -137,7 +137,11 @@ __global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState
 #ifndef PCB_U_VP
 #define PCB_U_VP 2
 #endif
-    constexpr int U = (FAM == kGaussian && MODE == kFromTable) ? PCB_U_VPG : PCB_U_VP;  // points in flight
+#ifndef PCB_U_VPU
+#define PCB_U_VPU 1
+#endif
+    // points in flight per thread (measured at C5: Gaussian 4, Frank 2, Gumbel 1)
+    constexpr int U = (FAM == kGaussian && MODE == kFromTable) ? PCB_U_VPG : (FAM == kGumbel ? PCB_U_VPU : PCB_U_VP);
     for (int k0 = 0; k0 < PPT; k0 += U) {
         unsigned long long p1[U], p2[U];  // packed ranks (by-row blocks)
         uint32_t w1[U], w2[U];            // route words (routed blocks)
