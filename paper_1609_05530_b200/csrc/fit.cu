@@ -38,7 +38,11 @@ constexpr int kMaxPasses = 64;
 // size d leaves an error ~C*d^2 (quadratic convergence): 1e-6 -> ~1e-12.
 constexpr double kTol64 = 1e-6;
 constexpr double kTol32 = 1e-6;
-constexpr int kWarmPasses = 2;  // fp32 warm-up passes before the fp64 passes (fp64 mode)
+constexpr int kWarmPasses = 2;
+#ifndef PCB_LIK_UNROLL
+#define PCB_LIK_UNROLL 4
+#endif
+constexpr int kLikUnroll = PCB_LIK_UNROLL;  // fp64 Newton pass: points per thread in flight  // fp32 warm-up passes before the fp64 passes (fp64 mode)
 
 // Spearman-rho -> theta inversion tables for the Archimedean init.
 constexpr int NTAB = 256;
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs,
 #ifndef PCB_U_PREP
 #define PCB_U_PREP 4
 #endif
-    constexpr int U = PCB_U_PREP;  // points per thread in flight
+    constexpr int U = FAM == kGumbel ? 2 : PCB_U_PREP;  // points per thread in flight (measured at C5)
     for (int k0 = 0; k0 < PPT; k0 += U) {
         double uu[U], ww[U], gx[U], gy[U];
         uint32_t ra[U], rb[U];
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
     if (sizeof(TI) == 16) {  // fp64
         if (FAM == kFrank) {
             const FrankTheta f(theta);
-#pragma unroll 4
+#pragma unroll(kLikUnroll)
             for (int k = 0; k < PPT; ++k) {
                 const uint32_t i = k * FT + threadIdx.x;
                 if (i < cnt) {
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
             }
         } else {
             const GumbelTheta g(theta);
-#pragma unroll 4
+#pragma unroll(kLikUnroll)
             for (int k = 0; k < PPT; ++k) {
                 const uint32_t i = k * FT + threadIdx.x;
                 if (i < cnt) {

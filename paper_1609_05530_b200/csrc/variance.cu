@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* seg
     const uint32_t base = (tile - S.tile0) * FTILE;
     double v[1] = {0.0};
 #ifndef PCB_U_FINAL
-#define PCB_U_FINAL 4
+#define PCB_U_FINAL 2
 #endif
     constexpr int U = PCB_U_FINAL;
     for (int k0 = 0; k0 < PPT; k0 += U) {
