@@ -379,7 +379,10 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
         }
     } else {  // fp32 per-point arithmetic: per-thread fp32 partial sums (PPT points), fp64 beyond
         float fs = 0.0f, fh = 0.0f;
-        constexpr int WB = 8;  // T32 loads in flight per thread
+#ifndef PCB_WB
+#define PCB_WB 8
+#endif
+        constexpr int WB = PCB_WB;  // T32 loads in flight per thread
         if (FAM == kFrank) {
             const FrankThetaF f(theta);
             for (int k0 = 0; k0 < PPT; k0 += WB) {
