@@ -137,7 +137,7 @@ struct RankBufs {
 
 RankBufs rank_buffers(pcb::Ctx& c, uint64_t n_rows, uint64_t n_seg) {
     RankBufs b;
-    b.r.rp = c.ws.get_t<unsigned long long>("pipe.rp", 2 * n_rows);
+    b.r.rp = nullptr;  // allocated by run_ranks only if some block needs by-row ranks
     b.bad = c.ws.get_t<int32_t>("pipe.bad", n_seg);
     PCB_CUDA(cudaMemsetAsync(b.bad, 0, n_seg * sizeof(int32_t), c.stream));
     return b;

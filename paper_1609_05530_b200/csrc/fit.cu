@@ -722,7 +722,8 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
     }
     void* T = (gtab && fam == kGaussian) ? nullptr
                                          : c.ws.get("fit.T", io.n_rows * (fp32T ? sizeof(float2) : sizeof(double2)));
-    float2* T32 = warm ? c.ws.get_t<float2>("fit.T32", io.n_rows) : nullptr;
+    // T32 (warm-up passes only) and the variance score zb share one 8-byte-per-row buffer
+    float2* T32 = warm ? c.ws.get_t<float2>("scratch.row8", io.n_rows) : nullptr;
     if (tiles > 0) {
         const int with_fit = io.do_fit ? 1 : 0;
         if (fam == kGaussian)

@@ -651,10 +651,8 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
                 bad[J.seg] = 1;
                 fb[jid] = 2;  // handled, no route
             }
-        } else if (constant) {  // one tie run: avg rank (n+1)/2 for all, stable positions = row order
-            for (uint32_t i = a + tid; i < e; i += CTT)
-                rp[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = pack_rank(J.n + 1u, i, i == 0);
-            if (r == 0 && tid == 0) fb[jid] = 2;  // ranked, no route
+        } else if (constant) {  // one tie run: avg rank (n+1)/2 for all; written by the host's pass (fb 3)
+            if (r == 0 && tid == 0) fb[jid] = 3;
         } else if (r == 0 && tid == 0) {
             fb[jid] = 1;
         }
@@ -1080,6 +1078,20 @@ void route_to_rows(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, const s
 
 }  // namespace
 
+// a constant column: one tie run, avg rank (n+1)/2, positions in row order
+__global__ void k_constant_rows(const ClusterJob* jobs, const uint32_t* list, uint64_t n_rows,
+                                unsigned long long* rp) {
+    const ClusterJob J = jobs[list[blockIdx.y]];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < J.n; i += gridDim.x * blockDim.x)
+        rp[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = pack_rank(J.n + 1u, i, i == 0);
+}
+
+// By-row packed ranks are only allocated when some block needs them (global
+// path, constant columns, PCB_VAR_GLOBAL): routed blocks never touch them.
+unsigned long long* rows_buffer(Ctx& c, uint64_t n_rows) {
+    return c.ws.get_t<unsigned long long>("pipe.rp", 2 * n_rows);
+}
+
 void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_rows, const std::vector<uint64_t>& off,
                RankOut& out, int32_t* d_bad) {
     const size_t K = off.size() - 1;
@@ -1123,13 +1135,28 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
             if (hfb[j]) out.routed[j % K] = 0;
             if (hfb[j] == 1) fallback.push_back(j);
         }
-        std::vector<uint32_t> convert;
-        for (uint32_t j = 0; j < njobs; ++j)
+        std::vector<uint32_t> convert, constant;
+        for (uint32_t j = 0; j < njobs; ++j) {
             if (hfb[j] == 0 && !out.routed[j % K]) convert.push_back(j);
+            if (hfb[j] == 3) constant.push_back(j);
+        }
+        if (!convert.empty() || !constant.empty() || !fallback.empty()) out.rp = rows_buffer(c, n_rows);
         if (!convert.empty()) route_to_rows(c, plan, jobs, convert, off, n_rows, out);
+        if (!constant.empty()) {
+            uint64_t nm = 0;
+            for (uint32_t j : constant) nm = std::max<uint64_t>(nm, hj[j].n);
+            auto* d_list = c.ws.get_t<uint32_t>("rank.constant", constant.size());
+            PCB_CUDA(cudaMemcpyAsync(d_list, constant.data(), constant.size() * sizeof(uint32_t),
+                                     cudaMemcpyHostToDevice, c.stream));
+            const dim3 grid(static_cast<unsigned>(std::min<uint64_t>(64, (nm + 255) / 256)),
+                            static_cast<unsigned>(constant.size()));
+            k_constant_rows<<<grid, 256, 0, c.stream>>>(jobs, d_list, n_rows, out.rp);
+            c.count_launch();
+        }
     } else {
         out.cl = 0;
         out.routed.assign(K, 0);
+        out.rp = rows_buffer(c, n_rows);
         for (uint32_t j = 0; j < 2 * K; ++j) fallback.push_back(j);
     }
     out.d_routed = c.ws.get_t<uint8_t>("rank.routed", K);

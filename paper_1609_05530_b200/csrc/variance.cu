@@ -636,7 +636,7 @@ void run_variance(Ctx& c, const VarIO& v) {
     const std::vector<uint64_t>& off = *v.off;
     const int K = static_cast<int>(off.size() - 1);
     const RankOut& R = *v.rank;
-    auto* zb = c.ws.get_t<double>("var.z", v.n_rows);
+    auto* zb = c.ws.get_t<double>("scratch.row8", v.n_rows);  // T32 is dead by now (fit.cu)
     // routed blocks (both columns ranked by the cluster path) reuse its route;
     // the others go through sorted-order arrays in global memory
     int nrouted = 0;
