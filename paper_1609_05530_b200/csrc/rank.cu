@@ -842,16 +842,22 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
             before += eqk && o < j;
         }
         const uint32_t llt = s0 + less;  // < T <= 16384, so local r2 = 2*llt + same + 1 <= 2T < 2^16
-        keep[k] = ((2u * llt + same + 1u) << 16) | (llt + before) | (before == 0 ? 0x8000u : 0u);
+        const uint32_t res = ((2u * llt + same + 1u) << 16) | (llt + before) | (before == 0 ? 0x8000u : 0u);
+        // full CTAs: outw[j] (this element's bucket) is read only by this thread,
+        // so the result replaces it at once; LEAN keeps it until the keys are dead
+        if constexpr (LEAN) keep[k] = res;
+        else outw[j] = res;
     }
     __syncthreads();
+    if constexpr (LEAN) {
 #pragma unroll
-    for (int k = 0; k < QM; ++k) {
-        const uint32_t qq = tid + k * CTT;
-        if (qq >= T) break;
-        outw[perm[qq]] = keep[k];
+        for (int k = 0; k < QM; ++k) {
+            const uint32_t qq = tid + k * CTT;
+            if (qq >= T) break;
+            outw[perm[qq]] = keep[k];
+        }
+        __syncthreads();
     }
-    __syncthreads();
     const uint64_t reg = ((static_cast<uint64_t>(J.col) * K + J.seg) * CL + r) * RCAP;
     if (tid == 0) ocnt[(static_cast<uint64_t>(J.col) * K + J.seg) * CL + r] = T;
     for (uint32_t j = tid; j < T; j += CTT) {  // coalesced, in slot order
