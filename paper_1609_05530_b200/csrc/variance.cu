@@ -260,8 +260,15 @@ __device__ __forceinline__ double finish_sigma2(BlockState& s, double zz, double
 //   scan:  thread t owns PT (odd: few bank conflicts) consecutive positions:
 //          thread sum -> block suffix of thread sums -> thread-serial suffix
 //   write: per slot, the suffix sum at its run start (bitmap search, local)
-constexpr int ST = 512;  // threads per scan CTA
-constexpr int SJ = 32;   // slots per thread (RCAP <= 16384)
+#ifndef PCB_SCAN_T
+#define PCB_SCAN_T 1024
+#endif
+#ifndef PCB_SCAN_B
+#define PCB_SCAN_B 8
+#endif
+constexpr int ST = PCB_SCAN_T;     // threads per scan CTA
+constexpr int SJ = 16384 / ST;     // slots per thread (RCAP <= 16384)
+constexpr int SB = PCB_SCAN_B < SJ ? PCB_SCAN_B : SJ;  // slot loads in flight per thread
 constexpr int SW = ST / 32;
 
 __global__ void __launch_bounds__(ST, 1) k_var_scan(const BlockState* st, const int* seg_list, int nseg,
@@ -295,10 +302,10 @@ __global__ void __launch_bounds__(ST, 1) k_var_scan(const BlockState* st, const 
     const uint16_t* P = posl + reg;
     // the first loads go out before the block's status and count arrive (the
     // region is RCAP slots long, so reading past the count is in bounds)
-    double x0[16];
-    uint32_t pv0[16];
+    double x0[SB];
+    uint32_t pv0[SB];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < SB; ++k) {
         const uint32_t j = tid + k * ST;
         if (j < RCAP) {
             pv0[k] = P[j];
@@ -312,16 +319,16 @@ __global__ void __launch_bounds__(ST, 1) k_var_scan(const BlockState* st, const 
     mark(0);
     uint32_t pk[SJ / 2];  // this thread's local positions (| run-start bit), two per register
 #pragma unroll
-    for (int h = 0; h < SJ; h += 16) {
+    for (int h = 0; h < SJ; h += SB) {
         if (tid + h * ST >= T) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) pk[(h >> 1) + k] = 0xffffffffu;
+            for (int k = 0; k < SB / 2; ++k) pk[(h >> 1) + k] = 0xffffffffu;
             continue;
         }
-        double x[16];
-        uint32_t pv[16];
+        double x[SB];
+        uint32_t pv[SB];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < SB; ++k) {
             const uint32_t j = tid + (h + k) * ST;
             if (h == 0) {
                 pv[k] = j < T ? pv0[k] : 0xffffu;
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(ST, 1) k_var_scan(const BlockState* st, const 
             }
         }
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < SB; ++k) {
             if (pv[k] != 0xffffu) {
                 const uint32_t p = pv[k] & 0x7fffu;
                 A[p] = x[k];
