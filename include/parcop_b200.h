@@ -103,7 +103,8 @@ uint64_t pcb_launch_count(const pcb_context* ctx);
 /* per-stage device milliseconds of the last pipeline call:
  * [0] rank [1] prepare+init [2] likelihood passes [3] variance [4] finalize
  * [5] fp64 likelihood-kernel ms and [6] its launches (inside [2])
- * [7] fp32 warm-up likelihood-kernel ms and [8] its launches (inside [2]);
+ * [7] fp32 warm-up likelihood-kernel ms and [8] its launches (inside [2])
+ * [9] variance pass 1 (per-point terms) ms (inside [3]);
  * returns the count written */
 int pcb_stage_times(const pcb_context* ctx, double* ms, int n);
 /* free cached device workspace */
