@@ -172,7 +172,10 @@ __global__ void k_init_state(BlockState* st, const Seg* segs, int nseg, const in
 // u only) holds the per-rank transform of the block's size: Phi^-1(u)
 // (Gaussian) or ln(-ln u) (Gumbel), bit-identical to computing it per point.
 template <int FAM, class TO>
-__global__ void __launch_bounds__(FT) k_prepare(BlockState* st, const Seg* segs, int nseg, RankRef R,
+#ifndef PCB_PREP_OCC
+#define PCB_PREP_OCC 0
+#endif
+__global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, const Seg* segs, int nseg, RankRef R,
                                                const double* __restrict__ u1, const double* __restrict__ u2,
                                                uint64_t n_rows, TO* __restrict__ T, float2* __restrict__ T32,
                                                const double* __restrict__ gtab, const uint64_t* goff,

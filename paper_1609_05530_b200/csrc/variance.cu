@@ -419,7 +419,10 @@ __global__ void k_var_carry(const int* seg_list, int njobs, int nseg, int CL, co
 }
 
 // z = score + W_1 + W_2 per row (through the route), sum z^2 -> sigma2
-__global__ void __launch_bounds__(FT) k_var_final(BlockState* st, const Seg* segs, int nseg, RankRef R,
+#ifndef PCB_FINAL_OCC
+#define PCB_FINAL_OCC 0
+#endif
+__global__ void __launch_bounds__(FT, PCB_FINAL_OCC) k_var_final(BlockState* st, const Seg* segs, int nseg, RankRef R,
                                                  uint64_t n_rows, const double* __restrict__ zb,
                                                  const double* __restrict__ xr, const double* __restrict__ carry,
                                                  double* partials, unsigned* tickets) {
