@@ -213,49 +213,89 @@ __global__ void __launch_bounds__(RT) k_hist(const RankRange* rr, int nr, const 
     }
 }
 
-// One block per range: exclusive scan of the range's bucket counts.
-__global__ void __launch_bounds__(1024) k_scan(const RankRange* rr, const uint32_t* hist, uint32_t* bstart,
-                                              uint32_t* cursor, Oversize* ov, uint32_t* ov_count,
-                                              uint32_t ov_cap) {
-    const RankRange R = rr[blockIdx.x];
-    __shared__ uint32_t s_warp[32];
-    __shared__ uint32_t s_carry;
-    if (threadIdx.x == 0) s_carry = 0;
+// Exclusive scan of every range's bucket counts in three phases over chunks
+// of SCH buckets (a range's bucket array may hold tens of millions of
+// buckets): chunk sums, per-range scan of the chunk sums, chunk scans.
+constexpr uint32_t SCH = 8192;
+struct ScanChunk {
+    uint32_t range, first;  // range index, first (range-local) bucket of the chunk
+};
+
+__global__ void __launch_bounds__(256) k_scan_sum(const RankRange* rr, const ScanChunk* ch, const uint32_t* hist,
+                                                 uint32_t* csum) {
+    const ScanChunk C = ch[blockIdx.x];
+    const RankRange R = rr[C.range];
+    const uint32_t end = min(C.first + SCH, R.nb);
+    uint32_t v = 0;
+    for (uint32_t b = C.first + threadIdx.x; b < end; b += blockDim.x) v += hist[R.bbase + b];
+    v = __reduce_add_sync(0xffffffffu, v);
+    __shared__ uint32_t s_w[8];
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
     __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < 8; ++w) t += s_w[w];
+        csum[blockIdx.x] = t;
+    }
+}
+
+// one thread per range: exclusive scan over its (consecutive) chunks
+__global__ void k_scan_off(int nr, const uint32_t* chunk0, const uint32_t* csum, uint32_t* coff) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nr) return;
+    uint32_t run = 0;
+    for (uint32_t c = chunk0[r]; c < chunk0[r + 1]; ++c) {
+        coff[c] = run;
+        run += csum[c];
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_apply(const RankRange* rr, const ScanChunk* ch, const uint32_t* hist,
+                                                    const uint32_t* coff, uint32_t* bstart, uint32_t* cursor,
+                                                    Oversize* ov, uint32_t* ov_count, uint32_t ov_cap) {
+    constexpr uint32_t PER = SCH / 1024;  // buckets per thread, consecutive
+    const ScanChunk C = ch[blockIdx.x];
+    const RankRange R = rr[C.range];
+    const uint32_t b0 = C.first + threadIdx.x * PER;
+    uint32_t c[PER], loc = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        c[k] = b0 + k < R.nb ? hist[R.bbase + b0 + k] : 0u;
+        loc += c[k];
+    }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (uint32_t base = 0; base < R.nb; base += blockDim.x) {
-        const uint32_t b = base + threadIdx.x;
-        const uint32_t c = b < R.nb ? hist[R.bbase + b] : 0u;
-        uint32_t x = c;  // inclusive warp scan
+    uint32_t x = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __shared__ uint32_t s_w[32];
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t z = s_w[lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += y;
         }
-        if (lane == 31) s_warp[w] = x;
-        __syncthreads();
-        if (w == 0) {
-            uint32_t z = lane < static_cast<int>(blockDim.x >> 5) ? s_warp[lane] : 0u;
+        s_w[lane] = z;
+    }
+    __syncthreads();
+    uint32_t run = coff[blockIdx.x] + (w ? s_w[w - 1] : 0u) + x - loc;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
-                if (lane >= o) z += y;
-            }
-            s_warp[lane] = z;
-        }
-        __syncthreads();
-        const uint32_t excl = s_carry + (w ? s_warp[w - 1] : 0u) + x - c;
+    for (int k = 0; k < PER; ++k) {
+        const uint32_t b = b0 + k;
         if (b < R.nb) {
-            bstart[R.bbase + b] = excl;
-            cursor[R.bbase + b] = excl;
-            if (c > CAP) {
+            bstart[R.bbase + b] = run;
+            cursor[R.bbase + b] = run;
+            if (c[k] > CAP) {
                 const uint32_t slot = atomicAdd(ov_count, 1u);
-                if (slot < ov_cap) ov[slot] = Oversize{blockIdx.x, excl, c, 0u};
+                if (slot < ov_cap) ov[slot] = Oversize{C.range, run, c[k], 0u};
             }
         }
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) s_carry = excl + c;
-        __syncthreads();
+        run += c[k];
     }
 }
 
@@ -979,7 +1019,26 @@ void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64
         k_resolve<<<(nr + 127) / 128, 128, 0, st>>>(d_rr, nr, l0 ? 1 : 0);
         if (l0) k_hist<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, hist);
         else k_hist<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, hist);
-        k_scan<<<nr, 1024, 0, st>>>(d_rr, hist, bstart, cursor, ov, ovn, ov_cap);
+        {  // chunked bucket scan
+            std::vector<ScanChunk> hc;
+            std::vector<uint32_t> c0(ranges.size() + 1);
+            for (size_t r = 0; r < ranges.size(); ++r) {
+                c0[r] = static_cast<uint32_t>(hc.size());
+                for (uint32_t f = 0; f < ranges[r].nb; f += SCH) hc.push_back(ScanChunk{static_cast<uint32_t>(r), f});
+            }
+            c0[ranges.size()] = static_cast<uint32_t>(hc.size());
+            const uint32_t nch = static_cast<uint32_t>(hc.size());
+            auto* d_ch = c.ws.get_t<ScanChunk>("rank.chunks", nch);
+            auto* d_c0 = c.ws.get_t<uint32_t>("rank.chunk0", c0.size());
+            auto* csum = c.ws.get_t<uint32_t>("rank.csum", nch);
+            auto* coff = c.ws.get_t<uint32_t>("rank.coff", nch);
+            PCB_CUDA(cudaMemcpyAsync(d_ch, hc.data(), nch * sizeof(ScanChunk), cudaMemcpyHostToDevice, st));
+            PCB_CUDA(cudaMemcpyAsync(d_c0, c0.data(), c0.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+            k_scan_sum<<<nch, 256, 0, st>>>(d_rr, d_ch, hist, csum);
+            k_scan_off<<<(nr + 127) / 128, 128, 0, st>>>(nr, d_c0, csum, coff);
+            k_scan_apply<<<nch, 1024, 0, st>>>(d_rr, d_ch, hist, coff, bstart, cursor, ov, ovn, ov_cap);
+            c.count_launch(2);
+        }
         if (l0) k_scatter<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
         else k_scatter<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
         k_rank<<<ntiles, RT, 0, st>>>(d_rr, nr, dkey, didx, hist, bstart, n_rows, out.rp);
