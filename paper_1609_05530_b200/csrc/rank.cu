@@ -4,10 +4,17 @@
 // (segment, column) the reference index-sorts by (value, index) and gives a
 // tie run i..j the average rank 0.5*((i+1)+(j+1)). The GPU never sorts:
 // ranking only needs, per element, lt = #{values < x} and eq = #{values == x}
-// in its segment (plus the number of equal values with a smaller row index,
-// which yields a unique stable position for the variance scatter).
+// in its segment (plus the number of equal values ordered before it, which
+// yields a unique position for the variance's suffix sums).
 //
-// Algorithm (one "level" = 6 launches over every range at once):
+// Two paths. Blocks a thread-block cluster can hold (C5: 125,000 rows) take
+// the cluster path (k_rank_cluster_t, below): an all-to-all over distributed
+// shared memory by value range, counting inside fine local buckets; ranks
+// stay per receive slot ("routed"). Larger blocks, skewed data and
+// non-finite ranges take the global path described here, which writes packed
+// ranks by row.
+//
+// Global path (one "level" = 8 launches over every range at once):
 //   minmax  per-range key / index extremes (64-bit order-preserving keys,
 //           -0.0 == +0.0), fused non-finite check (validate_data,
 //           pseudo_obs.hpp:30-37)
@@ -15,8 +22,9 @@
 //           row-index-linear for a range whose keys are all equal (a tie run)
 //   hist    bucket counts (monotone bucket map => buckets are ordered
 //           intervals of the sorted order; ties never straddle buckets)
-//   scan    per-range exclusive scan -> bucket starts; buckets above CAP are
-//           queued for the next level
+//   scan    per-range exclusive scan (chunk sums, per-range chunk offsets,
+//           chunk scans) -> bucket starts; buckets above CAP are queued for
+//           the next level
 //   scatter (key, row) into the bucket's slots of a scratch array
 //   rank    per element: count smaller / equal / equal-with-smaller-row
 //           inside its (small) bucket; lt = range base + bucket start + #less
