@@ -340,7 +340,10 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
 
 // One Newton pass: fused per-point score + Hessian at each running block's
 // current theta, deterministic block reduction, in-kernel Newton update.
-template <int FAM, class TI>
+// F32: fp32 per-point arithmetic (the warm-up passes, or the fp32 precision
+// mode); TI: the stored pair — float2 (T32 / fp32 T) or double2 (fp64 T,
+// converted at load: Frank to the edge encoding, Gumbel by rounding).
+template <int FAM, class TI, bool F32 = (sizeof(TI) == 8)>
 __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int nseg, const TI* __restrict__ T,
                                            double* partials, unsigned* tickets, unsigned* running, double tol) {
     const uint32_t tile = blockIdx.x;
@@ -352,7 +355,16 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
     const TI* Tb = T + S.begin + base;
     const uint32_t cnt = min(FTILE, S.n - base);
     double v[2] = {0.0, 0.0};
-    if (sizeof(TI) == 16) {  // fp64
+    auto warm_pair = [](const TI& p) -> float2 {
+        if constexpr (sizeof(TI) == 8) {
+            return p;
+        } else if constexpr (FAM == kFrank) {
+            return float2{frank_edge(p.x), frank_edge(p.y)};
+        } else {
+            return float2{static_cast<float>(p.x), static_cast<float>(p.y)};
+        }
+    };
+    if constexpr (!F32) {  // fp64
         if (FAM == kFrank) {
             const FrankTheta f(theta);
 #pragma unroll(kLikUnroll)
@@ -399,7 +411,7 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
               for (int u = 0; u < WB; ++u) {
                 const uint32_t i = (k0 + u) * FT + threadIdx.x;
                 if (i < cnt) {
-                    const TI p = pb[u];
+                    const float2 p = warm_pair(pb[u]);
                     float uv, uc, vv, vc;
                     frank_unedge(p.x, uv, uc);
                     frank_unedge(p.y, vv, vc);
@@ -438,7 +450,8 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
                 const uint32_t i = (k0 + u) * FT + threadIdx.x;
                 if (i < cnt) {
                     float s, h;
-                    gumbel_sh_f(pb[u].x, pb[u].y, g, s, h);
+                    const float2 p = warm_pair(pb[u]);
+                    gumbel_sh_f(p.x, p.y, g, s, h);
                     fs += s;
                     fh += h;
                 }
@@ -599,8 +612,11 @@ void launch_prepare(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int
 
 template <int FAM>
 void launch_lik(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, bool f32, const void* T,
-                double* part, unsigned* tick, unsigned* running, double tol) {
-    if (f32)
+                double* part, unsigned* tick, unsigned* running, double tol, bool t64 = false) {
+    if (f32 && t64)  // fp32 warm-up arithmetic straight from the fp64 T
+        k_lik<FAM, double2, true><<<tiles, FT, 0, c.stream>>>(st, segs, K, static_cast<const double2*>(T), part,
+                                                              tick, running, tol);
+    else if (f32)
         k_lik<FAM, float2><<<tiles, FT, 0, c.stream>>>(st, segs, K, static_cast<const float2*>(T), part, tick,
                                                        running, tol);
     else
@@ -725,8 +741,12 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
     }
     void* T = (gtab && fam == kGaussian) ? nullptr
                                          : c.ws.get("fit.T", io.n_rows * (fp32T ? sizeof(float2) : sizeof(double2)));
-    // T32 (warm-up passes only) and the variance score zb share one 8-byte-per-row buffer
-    float2* T32 = warm ? c.ws.get_t<float2>("scratch.row8", io.n_rows) : nullptr;
+    // T32 (warm-up passes only) and the variance score zb share one 8-byte-per-row buffer.
+    // Gumbel's warm-up passes read the fp64 T directly (no T32: measured faster
+    // overall); PCB_WARM_FROM_T=0/1 forces either way for both families
+    const char* wft = std::getenv("PCB_WARM_FROM_T");
+    const bool warm_t64 = warm && !fp32T && (wft && wft[0] ? wft[0] != '0' : fam == kGumbel);
+    float2* T32 = (warm && !warm_t64) ? c.ws.get_t<float2>("scratch.row8", io.n_rows) : nullptr;
     if (tiles > 0) {
         const int with_fit = io.do_fit ? 1 : 0;
         if (fam == kGaussian)
@@ -749,11 +769,12 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
         for (int pass = 0; pass < kMaxPasses; ++pass) {
             const bool wp = warm && pass < kWarmPasses;
             const bool f32 = wp || fp32T;
-            const void* Tp = wp ? static_cast<const void*>(T32) : T;
+            const void* Tp = (wp && !warm_t64) ? static_cast<const void*>(T32) : T;
             const double tol = wp ? -1.0 : (fp32T ? kTol32 : kTol64);
+            const bool t64 = wp && warm_t64;
             PCB_CUDA(cudaEventRecord(ev[6], s));
-            if (fam == kFrank) launch_lik<kFrank>(c, tiles, st, d_segs, K, f32, Tp, part, tick, running, tol);
-            else launch_lik<kGumbel>(c, tiles, st, d_segs, K, f32, Tp, part, tick, running, tol);
+            if (fam == kFrank) launch_lik<kFrank>(c, tiles, st, d_segs, K, f32, Tp, part, tick, running, tol, t64);
+            else launch_lik<kGumbel>(c, tiles, st, d_segs, K, f32, Tp, part, tick, running, tol, t64);
             PCB_CUDA(cudaEventRecord(ev[7], s));
             PCB_CUDA(cudaMemcpyAsync(h_running, running, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
             PCB_CUDA(cudaStreamSynchronize(s));
