@@ -107,6 +107,10 @@ uint64_t pcb_launch_count(const pcb_context* ctx);
  * [9] variance pass 1 (per-point terms) ms (inside [3]);
  * returns the count written */
 int pcb_stage_times(const pcb_context* ctx, double* ms, int n);
+/* block columns (2 per block) of the last rank stage by path: [0] cluster
+ * kernel (one thread-block cluster per column), [1] global multi-level
+ * bucket path, [2] constant column, [3] non-finite (rejected) */
+int pcb_rank_paths(const pcb_context* ctx, uint64_t counts[4]);
 /* free cached device workspace */
 int pcb_trim(pcb_context* ctx);
 

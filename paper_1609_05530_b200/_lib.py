@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("PCB_LIB_PATH") or os.path.join(HERE, "libparcop_b200.
 # Every symbol include/parcop_b200.h declares (tests check the export table).
 SYMBOLS = (
     "pcb_create", "pcb_destroy", "pcb_last_error", "pcb_abi_version", "pcb_set_stream", "pcb_launch_count",
-    "pcb_stage_times", "pcb_trim", "pcb_normalized_ranks", "pcb_pseudo_loglik", "pcb_fit",
+    "pcb_stage_times", "pcb_rank_paths", "pcb_trim", "pcb_normalized_ranks", "pcb_pseudo_loglik", "pcb_fit",
     "pcb_asymptotic_variance", "pcb_partition", "pcb_combine", "pcb_fit_blocks", "pcb_fit_parallel", "pcb_sample",
     "pcb_measure_fp64_peak", "pcb_rel_error", "pcb_cdf", "pcb_spearman_rho", "pcb_kendall_tau",
     "pcb_model_kendall_tau", "pcb_inverse_tau",
@@ -69,6 +69,7 @@ def load():
         "pcb_set_stream": ([vp, vp], i),
         "pcb_launch_count": ([vp], u64),
         "pcb_stage_times": ([vp, P(d), i], i),
+        "pcb_rank_paths": ([vp, P(u64)], i),
         "pcb_trim": ([vp], i),
         "pcb_normalized_ranks": ([vp, vp, vp, u64, P(u64), u64, vp, vp], i),
         "pcb_pseudo_loglik": ([vp, i, vp, vp, vp, u64, P(u64), u64, vp], i),

@@ -299,6 +299,12 @@ int pcb_stage_times(const pcb_context* ctx, double* ms, int n) {
     return k;
 }
 
+int pcb_rank_paths(const pcb_context* ctx, uint64_t* counts) {
+    if (!ctx || !counts) return PCB_E_INVALID;
+    for (int i = 0; i < 4; ++i) counts[i] = ctx->c.rank_paths[i];
+    return PCB_OK;
+}
+
 int pcb_trim(pcb_context* ctx) {
     return guarded(ctx, [&] {
         PCB_CUDA(cudaStreamSynchronize(ctx->c.stream));

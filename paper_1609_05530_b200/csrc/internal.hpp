@@ -67,6 +67,9 @@ struct Ctx {
     uint64_t launches = 0;
     double stage_ms[12] = {0};
     int n_stage = 0;
+    // block columns of the last rank stage by path: [0] cluster, [1] global,
+    // [2] constant, [3] invalid (non-finite)
+    uint64_t rank_paths[4] = {0, 0, 0, 0};
     cudaEvent_t ev[8] = {};
     cudaStream_t copy_stream = nullptr;  // host->device streaming of inputs (overlaps compute)
     cudaEvent_t cev[4] = {};

@@ -483,6 +483,46 @@ inline ClusterPlan plan_cluster(uint64_t nmax) {
     return ClusterPlan{};
 }
 
+// Quantile-knot map for skewed blocks (the cluster kernel's second pass):
+// kn[0..nk) sorted knot keys with kn[0] <= k, cm[j] = elements before
+// interval j (exact, cluster-wide). Interval i = [kn[i], kn[i+1]); the last
+// one holds the keys equal to the maximum. Explicit roundings: every CTA
+// computes the same position for the same key.
+// Knot tables are stored with one pad slot per 16 keys (kpad), so the
+// search's power-of-two strides do not all land in one shared-memory bank.
+__device__ __forceinline__ uint32_t kpad(uint32_t i) { return i + (i >> 4); }
+// Intervals of N keys at once (kn padded with ~0ull, above every finite key,
+// to 2^LG entries): a fixed-step search, step-major so the N chains of
+// dependent shared loads overlap. Interval = (knots <= k) - 1, >= 0 when kn[0] <= k.
+template <int LG, int N>
+__device__ __forceinline__ void qsearch(const unsigned long long* kn, const unsigned long long (&k)[N],
+                                        uint32_t (&iv)[N]) {
+    uint32_t p[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) p[u] = 0;
+#pragma unroll
+    for (uint32_t h = 1u << (LG - 1); h > 0; h >>= 1)
+#pragma unroll
+        for (int u = 0; u < N; ++u)
+            if (kn[kpad(p[u] + h - 1)] <= k[u]) p[u] += h;
+#pragma unroll
+    for (int u = 0; u < N; ++u) iv[u] = p[u] ? p[u] - 1 : 0;
+}
+// Interpolated position g in [0, N] of key k in interval i: cm[i] plus
+// min(c_i, (k - kn[i]) * sl[i]), sl[i] = c_i / (kn[i+1] - kn[i]) in halved
+// values (0 for the last, maximum-equal interval). Monotone in k across
+// intervals (g <= cm[i+1] inside interval i).
+__device__ __forceinline__ double qpos(unsigned long long k, uint32_t i, const unsigned long long* kn,
+                                       const uint32_t* cm, const double* sl) {
+    const double v = __dmul_rn(0.5, key_value(k)), q0 = __dmul_rn(0.5, key_value(kn[kpad(i)]));
+    const double c = static_cast<double>(cm[i + 1] - cm[i]);
+    const double t = fmin(c, fmax(0.0, __dmul_rn(__dsub_rn(v, q0), sl[i])));  // NaN (0 * inf) -> 0
+    return __dadd_rn(static_cast<double>(cm[i]), t);
+}
+__device__ __forceinline__ uint32_t qbucket(double g, double qs, uint32_t nbtot) {
+    return min(nbtot - 1u, static_cast<uint32_t>(__dmul_rn(g, qs)));
+}
+
 __device__ __forceinline__ uint32_t cbucket(unsigned long long k, double hm, double scale, uint32_t nbtot) {
     const double t = (0.5 * key_value(k) - hm) * scale;  // monotone in k; clamped at both ends
     return t > 0.0 ? (t < static_cast<double>(nbtot) ? static_cast<uint32_t>(t) : nbtot - 1u) : 0u;
@@ -708,76 +748,256 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         return;
     }
 
-    // ---- 2. per-warp counts of what this CTA sends to each value-range owner;
-    // each element's global bucket is kept (16 bits, two per register)
+    // ---- 2. per-warp counts of what this CTA sends to each value-range owner.
+    // Pass 0 splits [min, max] value-linearly (balanced for uniform-like data,
+    // e.g. pseudo-observations). If an owner would overflow its receive buffer
+    // (skewed raw marginals: normal, exponential, heavy tails), full CTAs in
+    // tail mode re-split by exact quantile knots and count again (pass 1);
+    // only if that still overflows does the block take the global path.
+    auto kclamp = [&](unsigned long long k) { return k < s_gmin ? s_gmin : (k > s_gmax ? s_gmax : k); };
+    constexpr uint32_t NKMAX = 512;  // quantile knots (sample + exact extremes), < NKMAX used
+    constexpr uint32_t SUBK = 128;   // an owner's share of the knot table (< SUBK - 1 intervals)
+    // quantile mode tables in the receive buffer (idle until the send phase),
+    // in u64 slots: [0,512) own sample (read by peers) | [512,1536) gathered
+    // sample / sort exchange | [1536,2080) knots (kpad) | [2080,2336) own
+    // interval counts (u32, read by peers) | [2336,2593) cums (u32) |
+    // [2600,3112) slopes (f64) | [QTAB, +S/4) interval id per element (u16).
+    // The owner's share (knots, cums, slopes) sits in the last SUBSLOTS
+    // slots, which the send never reaches in this mode (totals <= RCAP - SUBSLOTS).
+    constexpr uint32_t SUBSLOTS = (SUBK + SUBK / 16) + (SUBK / 2 + 1) + SUBK;
+    constexpr uint32_t QTAB = 3200;
+    __shared__ uint32_t s_ilo[kMaxCluster], s_ihi[kMaxCluster], s_qbad;
+    __shared__ double s_qs;  // nbtot / N
+    bool qmode = false;
+    unsigned long long* const knot = recv_key + 1536;
+    uint32_t* const cum = reinterpret_cast<uint32_t*>(recv_key + 2336);
+    double* const slope = reinterpret_cast<double*>(recv_key + 2600);
+    unsigned long long* const sk = recv_key + (RCAP - SUBSLOTS);  // owner share
+    uint32_t* const sc = reinterpret_cast<uint32_t*>(sk + SUBK + SUBK / 16);
+    double* const ssl = reinterpret_cast<double*>(sk + SUBK + SUBK / 16 + SUBK / 2 + 1);
+    uint16_t* const ivs = reinterpret_cast<uint16_t*>(recv_key + QTAB);  // interval id per slice element
     uint32_t bk[EMAX / 8];  // owner (4 bits) per element
-#pragma unroll
-    for (int k = 0; k < EMAX / 8; ++k) bk[k] = 0u;
-    bool fin = true;
     wait_slice();  // the mbarrier was initialised before the first __syncthreads
+    for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
-    for (int k = 0; k < EMAX; ++k) {
-        const uint32_t i = a + k * CTT + tid;
-        if (i < e) {
-            const double v = xs[i];
-            fin &= isfinite(v);
-            const uint32_t b = cbucket(order_key(v), hm, scale, nbtot);
-            bk[k >> 3] |= (b >> lg_nbl) << ((k & 7) * 4);
-            atomicAdd(&s_wc[wid][b >> lg_nbl], 1u);
-        }
-    }
-    if (!__syncthreads_and(fin) && tid == 0) s_bad = 1;  // validate_data (pseudo_obs.hpp:34-36)
-    if (tid < CL) {  // totals per owner, and per-warp exclusive bases
-        uint32_t run = 0;
-        for (int w = 0; w < (CTT / 32); ++w) {
-            const uint32_t c = s_wc[w][tid];
-            s_wc[w][tid] = run;
-            run += c;
-        }
-        s_cnt[tid] = run;
-    }
-    cluster.sync();
-    mark(1);
-    if (tid < CL * CL) s_mat[tid] = *cluster.map_shared_rank(&s_cnt[tid % CL], tid / CL);  // [src][dst]
-    if (wid == 1) {
-        const int gb = __any_sync(0xffffffffu, lane < CL && *cluster.map_shared_rank(&s_bad, lane) != 0);
-        if (lane == 0) s_gbad = gb;
-    }
-    __syncthreads();
-    if (s_gbad) {
-        if (r == 0 && tid == 0) {
-            bad[J.seg] = 1;
-            fb[jid] = 2;
-        }
-        cluster.sync();
-        return;
-    }
-    if (wid == 0) {  // lane d: owner d's receive total and this CTA's offset in it
-        uint32_t col = 0, mine = 0;
-        if (lane < CL)
-            for (int q = 0; q < CL; ++q) {
-                const uint32_t v = s_mat[q * CL + lane];
-                col += v;
-                if (q < r) mine += v;
+        for (int k = 0; k < EMAX / 8; ++k) bk[k] = 0u;
+        bool fin = true;
+#pragma unroll
+        for (int k = 0; k < EMAX; ++k) {
+            const uint32_t i = a + k * CTT + tid;
+            if (i < e) {
+                const double v = xs[i];
+                fin &= isfinite(v);
+                const unsigned long long kk = order_key(v);
+                const uint32_t d = (qmode ? qbucket(qpos(kk, ivs[i - a], knot, cum, slope), s_qs, nbtot)
+                                          : cbucket(kk, hm, scale, nbtot)) >> lg_nbl;
+                bk[k >> 3] |= d << ((k & 7) * 4);
             }
-        if (lane < CL) s_off[lane] = mine;
-        const bool over = __any_sync(0xffffffffu, lane < CL && col > RCAP);
-        uint32_t below = lane < r ? col : 0u;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
-        const uint32_t total = __shfl_sync(0xffffffffu, col, r);
-        if (lane == 0) {
-            s_total = total;
-            s_base = below;
-            s_over = over;
         }
-    }
-    __syncthreads();
-    if (s_over) {
-        if (r == 0 && tid == 0) fb[jid] = 1;
+#pragma unroll
+        for (int k = 0; k < EMAX; ++k)  // the counts after all the (independent) owner lookups
+            if (a + k * CTT + tid < e) atomicAdd(&s_wc[wid][(bk[k >> 3] >> ((k & 7) * 4)) & 0xfu], 1u);
+        if (!__syncthreads_and(fin) && tid == 0) s_bad = 1;  // validate_data (pseudo_obs.hpp:34-36)
+        if (tid < CL) {  // totals per owner, and per-warp exclusive bases
+            uint32_t run = 0;
+            for (int w = 0; w < (CTT / 32); ++w) {
+                const uint32_t c = s_wc[w][tid];
+                s_wc[w][tid] = run;
+                run += c;
+            }
+            s_cnt[tid] = run;
+        }
         cluster.sync();
-        mark(2);
-        return;
+        mark(1);
+        if (tid < CL * CL) s_mat[tid] = *cluster.map_shared_rank(&s_cnt[tid % CL], tid / CL);  // [src][dst]
+        if (wid == 1) {
+            const int gb = __any_sync(0xffffffffu, lane < CL && *cluster.map_shared_rank(&s_bad, lane) != 0);
+            if (lane == 0) s_gbad = gb;
+        }
+        __syncthreads();
+        if (s_gbad) {
+            if (r == 0 && tid == 0) {
+                bad[J.seg] = 1;
+                fb[jid] = 2;
+            }
+            cluster.sync();
+            return;
+        }
+        const uint32_t cap = qmode ? RCAP - SUBSLOTS : RCAP;
+        if (wid == 0) {  // lane d: owner d's receive total and this CTA's offset in it
+            uint32_t col = 0, mine = 0;
+            if (lane < CL)
+                for (int q = 0; q < CL; ++q) {
+                    const uint32_t v = s_mat[q * CL + lane];
+                    col += v;
+                    if (q < r) mine += v;
+                }
+            if (lane < CL) s_off[lane] = mine;
+            const bool over = __any_sync(0xffffffffu, lane < CL && col > cap);
+            uint32_t below = lane < r ? col : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+            const uint32_t total = __shfl_sync(0xffffffffu, col, r);
+            if (lane == 0) {
+                s_total = total;
+                s_base = below;
+                s_over = over;
+            }
+        }
+        __syncthreads();
+        if (!s_over) break;
+        if (LEAN || !tail || pass == 1 || RCAP < QTAB + (S + 3) / 4 + SUBSLOTS) {  // the global path takes the block
+            if (r == 0 && tid == 0) fb[jid] = 1;
+            cluster.sync();
+            mark(2);
+            return;
+        }
+        // ---- skewed block: equal-count owners from quantile knots. Knots =
+        // exact extremes + a strided sample of every slice, sorted identically
+        // in every CTA; exact cluster-wide counts per knot interval; positions
+        // interpolate linearly inside an interval (~N/NK elements each), so
+        // owners balance to within a few elements and local buckets stay
+        // ~N/nbtot deep whatever the marginal.
+        const uint32_t m = (NKMAX - 3) / CL;  // sample per CTA (knots < NKMAX for the fixed-step search)
+        const uint32_t len = e - a;
+        kmn = ~0ull;
+        kmx = 0ull;
+        for (uint32_t i = a + tid; i < e; i += CTT) {
+            const unsigned long long kk = order_key(xs[i]);
+            kmn = min(kmn, kk);
+            kmx = max(kmx, kk);
+        }
+        if (tid < m) recv_key[tid] = len ? order_key(xs[a + static_cast<uint32_t>((static_cast<uint64_t>(tid) * len) / m)])
+                                         : 0ull;  // empty slice: clamped to the minimum below
+        uint32_t* const hc = reinterpret_cast<uint32_t*>(recv_key + 2080);
+        for (uint32_t q = tid; q < NKMAX; q += CTT) hc[q] = 0u;
+        if (tid < CL) {
+            s_ilo[tid] = ~0u;
+            s_ihi[tid] = 0u;
+        }
+        if (tid == 0) s_qbad = 0;
+        cta_extremes();  // exact slice extremes -> s_rmin/s_rmax
+        cluster.sync();  // samples and extremes visible; every peer is done with the first matrix
+        cluster_extremes();
+        const uint32_t ns = m * CL, nk = ns + 2;
+        unsigned long long* const raw = recv_key + 512;
+        for (uint32_t j = tid; j < ns; j += CTT)
+            raw[j] = kclamp(*cluster.map_shared_rank(recv_key + j % m, j / m));
+        __syncthreads();
+        {  // bitonic sort of the ns < NKMAX samples, one per thread (pads sort last)
+            unsigned long long v = static_cast<uint32_t>(tid) < ns ? raw[tid] : ~0ull;
+            unsigned long long* const xb = raw;  // exchange buffer (each thread read only its own slot)
+            for (uint32_t kb = 2; kb <= NKMAX; kb <<= 1)  // threads >= NKMAX sort pads alongside
+                for (uint32_t j = kb >> 1; j > 0; j >>= 1) {
+                    unsigned long long pv;
+                    if (j >= 32) {
+                        xb[tid] = v;
+                        __syncthreads();
+                        pv = xb[tid ^ j];
+                        __syncthreads();
+                    } else {
+                        pv = __shfl_xor_sync(0xffffffffu, v, j);
+                    }
+                    const bool up = (tid & kb) == 0, low = (tid & j) == 0;
+                    v = (low == up) ? min(v, pv) : max(v, pv);
+                }
+            if (tid + 1 < static_cast<int>(NKMAX)) knot[kpad(1 + tid)] = v;  // knot[1 + ns ..]: pads (~0ull)
+        }
+        __syncthreads();
+        if (tid == 0) {
+            knot[0] = s_gmin;
+            knot[kpad(nk - 1)] = s_gmax;
+        }
+        __syncthreads();
+        mark(6);
+        for (uint32_t i0 = a + tid; i0 < e; i0 += 8 * CTT) {  // this slice's count per interval
+            unsigned long long kk[8];
+            uint32_t iv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = i0 + u * CTT;
+                kk[u] = i < e ? order_key(xs[i]) : 0ull;
+            }
+            qsearch<9>(knot, kk, iv);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i0 + u * CTT < e) {
+                    ivs[i0 + u * CTT - a] = static_cast<uint16_t>(iv[u]);
+                    atomicAdd(hc + iv[u], 1u);
+                }
+        }
+        mark(8);
+        cluster.sync();  // every CTA's interval counts are final
+        mark(9);
+        {
+            uint32_t c = 0;  // thread t: interval t, summed over the cluster (loads in flight together)
+            if (static_cast<uint32_t>(tid) < nk)
+                for (int q = 0; q < CL; ++q) c += *cluster.map_shared_rank(hc + tid, q);
+            uint32_t x2 = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x2, o);
+                if (lane >= o) x2 += y;
+            }
+            if (lane == 31) s_w[wid] = x2;
+            __syncthreads();
+            if (wid == 0) {
+                uint32_t z = lane < (CTT / 32) ? s_w[lane] : 0u;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+                    if (lane >= o) z += y;
+                }
+                if (lane < (CTT / 32)) s_w[lane] = z;
+            }
+            __syncthreads();
+            const uint32_t incl = (wid ? s_w[wid - 1] : 0u) + x2;
+            if (static_cast<uint32_t>(tid) < nk) cum[tid + 1] = incl;
+            if (tid == 0) cum[0] = 0u;
+        }
+        __syncthreads();
+        const double qs = static_cast<double>(nbtot) / static_cast<double>(cum[nk]);
+        if (tid == 0) s_qs = qs;
+        if (static_cast<uint32_t>(tid) < nk) {  // interval slopes (halved values; 0 for the last)
+            const uint32_t cc = cum[tid + 1] - cum[tid];
+            double sv = 0.0;
+            if (static_cast<uint32_t>(tid) + 1 < nk && cc) {
+                const double q0 = __dmul_rn(0.5, key_value(knot[kpad(tid)]));
+                const double q1 = __dmul_rn(0.5, key_value(knot[kpad(tid + 1)]));
+                sv = __ddiv_rn(static_cast<double>(cc), __dsub_rn(q1, q0));  // +inf for an underflowed width
+            }
+            slope[tid] = sv;
+        }
+        if (static_cast<uint32_t>(tid) < nk) {  // owners that interval tid can reach
+            const uint32_t o0 = qbucket(static_cast<double>(cum[tid]), qs, nbtot) >> lg_nbl;
+            const uint32_t o1 = qbucket(static_cast<double>(cum[tid + 1]), qs, nbtot) >> lg_nbl;
+            for (uint32_t o = o0; o <= o1; ++o) {
+                atomicMin(&s_ilo[o], static_cast<uint32_t>(tid));
+                atomicMax(&s_ihi[o], static_cast<uint32_t>(tid));
+            }
+        }
+        __syncthreads();
+        if (tid < CL && s_ilo[tid] != ~0u && s_ihi[tid] - s_ilo[tid] + 1 > SUBK - 2) s_qbad = 1;
+        __syncthreads();
+        mark(10);
+        if (s_qbad) {  // same decision in every CTA (same tables)
+            if (r == 0 && tid == 0) fb[jid] = 1;
+            cluster.sync();
+            mark(2);
+            return;
+        }
+        if (s_ilo[r] != ~0u) {  // this owner's share: knots ilo.., cums ilo..ihi+1
+            const uint32_t ilo = s_ilo[r], nint = s_ihi[r] - ilo + 1;
+            for (uint32_t q = tid; q < SUBK; q += CTT) {
+                sk[kpad(q)] = q <= nint && ilo + q < nk ? knot[kpad(ilo + q)] : ~0ull;
+                if (q <= nint) sc[q] = cum[ilo + q];
+                ssl[q] = q < nint ? slope[ilo + q] : 0.0;
+            }
+        }
+        for (int q = tid; q < (CTT / 32) * kMaxCluster; q += CTT) (&s_wc[0][0])[q] = 0u;
+        __syncthreads();
+        qmode = true;
+        mark(7);
     }
     for (int q = tid; q < (CTT / 32) * CL; q += CTT) s_wc[q / CL][q % CL] += s_off[q % CL];
     __syncthreads();
@@ -850,8 +1070,25 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
             perm[lhs[keep[k2] & 0x3fffu] + (keep[k2] >> 14)] = static_cast<uint16_t>(j);
         }
     } else {
+        // quantile mode: positions from the owner's share of the knot table (the senders' values)
+        const uint32_t b0 = static_cast<uint32_t>(r) << lg_nbl;
+        if (qmode)  // local buckets first (independent searches), kept in outw until the counting below
+            for (uint32_t j0 = tid; j0 < T; j0 += 4 * CTT) {
+                unsigned long long kq[4];
+                uint32_t iv[4], lv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) kq[u] = j0 + u * CTT < T ? recv_key[j0 + u * CTT] : 0ull;
+                qsearch<7>(sk, kq, iv);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    lv[u] = min(lmask, qbucket(qpos(kq[u], iv[u], sk, sc, ssl), s_qs, nbtot) - b0);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (j0 + u * CTT < T) outw[j0 + u * CTT] = lv[u];
+            }
         for (uint32_t j = tid; j < T; j += CTT) {
-            const uint32_t lb = cbucket(recv_key[j], hm, scale, nbtot) & lmask, sh = (lb & 1) * 16;
+            const uint32_t lb = qmode ? outw[j] : (cbucket(recv_key[j], hm, scale, nbtot) & lmask);
+            const uint32_t sh = (lb & 1) * 16;
             const uint32_t idx = (atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu;
             outw[j] = lb | (idx << 14);
         }
@@ -944,20 +1181,21 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
     cfg.numAttrs = 1;
     unsigned long long* prof = nullptr;
     if (getenv_flag("PCB_RANK_PROFILE")) {
-        prof = c.ws.get_t<unsigned long long>("rank.prof", 8);
-        PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
+        prof = c.ws.get_t<unsigned long long>("rank.prof", 12);
+        PCB_CUDA(cudaMemsetAsync(prof, 0, 12 * sizeof(unsigned long long), c.stream));
     }
     PCB_CUDA(cudaLaunchKernelEx(&cfg, kern, jobs, c0, c1, n_rows, out.rp, out.route, out.r2s, out.posl,
                                 out.ocnt,
                                 njobs / 2, fb, bad, p.cl, p.rcap, p.lg_nbl, tail, prof));
     if (prof) {
-        unsigned long long h[8];
+        unsigned long long h[12];
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
         PCB_CUDA(cudaStreamSynchronize(c.stream));
         const double ctas = static_cast<double>(njobs) * p.cl;
         std::fprintf(stderr, "[rank profile] CL=%d S=%u lean=%d: cycles/CTA  minmax %.0f  count %.0f  matrix %.0f  "
-                     "send %.0f  localsort %.0f  rank %.0f\n", p.cl, p.s, int(p.lean), h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
-                     h[4] / ctas, h[5] / ctas);
+                     "send %.0f  localsort %.0f  rank %.0f  qsample+sort %.0f  qhist-loop %.0f  qhist-sync %.0f  qcum %.0f  "
+                     "qshare %.0f\n", p.cl, p.s, int(p.lean), h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
+                     h[4] / ctas, h[5] / ctas, h[6] / ctas, h[8] / ctas, h[9] / ctas, h[10] / ctas, h[7] / ctas);
     }
     c.count_launch();
 }
@@ -1176,6 +1414,7 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
         nmax = std::max(nmax, n);
     }
     std::vector<uint32_t> fallback;
+    for (auto& v : c.rank_paths) v = 0;
     ClusterPlan plan = plan_cluster(nmax);
     if (plan.cl > 0 && !getenv_flag("PCB_RANK_GLOBAL")) {
         const uint32_t njobs = static_cast<uint32_t>(2 * K);
@@ -1207,6 +1446,7 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
         for (uint32_t j = 0; j < njobs; ++j) {
             if (hfb[j]) out.routed[j % K] = 0;
             if (hfb[j] == 1) fallback.push_back(j);
+            ++c.rank_paths[hfb[j] == 0 ? 0 : hfb[j] == 1 ? 1 : hfb[j] == 3 ? 2 : 3];
         }
         std::vector<uint32_t> convert, constant;
         for (uint32_t j = 0; j < njobs; ++j) {
@@ -1232,6 +1472,7 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
         out.rp = rows_buffer(c, n_rows);
         for (uint32_t j = 0; j < 2 * K; ++j) fallback.push_back(j);
     }
+    if (out.cl == 0) c.rank_paths[1] = 2 * K;
     out.d_routed = c.ws.get_t<uint8_t>("rank.routed", K);
     PCB_CUDA(cudaMemcpyAsync(out.d_routed, out.routed.data(), K, cudaMemcpyHostToDevice, c.stream));
     run_ranks_global(c, d_col1, d_col2, n_rows, off, fallback, out, d_bad);

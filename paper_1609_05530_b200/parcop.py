@@ -178,6 +178,12 @@ class Context:
                  "warm_kernel_ms", "warm_launches", "var_point_ms"]
         return {names[i]: float(buf[i]) for i in range(k)}
 
+    def rank_paths(self) -> dict:
+        """Block columns of the last rank stage by path (cluster / global / constant / invalid)."""
+        buf = (C.c_uint64 * 4)()
+        self.check(self.lib.pcb_rank_paths(self.ptr, buf))
+        return dict(zip(("cluster", "global", "constant", "invalid"), (int(v) for v in buf)))
+
     def trim(self):
         self.check(self.lib.pcb_trim(self.ptr))
 

@@ -6,6 +6,7 @@ likelihood path) of the CPU oracle on the same bytes.
 """
 import numpy as np
 import pytest
+from scipy.special import ndtri
 
 import paper_1609_05530_b200 as pcb
 
@@ -290,6 +291,51 @@ def test_rank_large_and_cluster_segments(ctx, orc, n, k):
     U = pcb.normalized_ranks(pcb.DataMatrix(c1, c2), off, ctx=ctx)
     assert np.array_equal(U.u1, oracle_ranks(orc, c1, off))
     assert np.array_equal(U.u2, oracle_ranks(orc, c2, off))
+
+
+SKEWED = {
+    "normal": lambda u: ndtri(u),
+    "exponential": lambda u: -np.log1p(-u),
+    "cauchy": lambda u: np.tan(np.pi * (u - 0.5)),
+    "lognormal": lambda u: np.exp(3.0 * ndtri(u)),
+    "narrow-offset": lambda u: 1000.0 + 1e-3 * ndtri(u),
+    "mixed-sign-pareto": lambda u: np.sign(u - 0.5) * (np.abs(2.0 * u - 1.0) + 1e-12) ** -1.5,
+}
+
+
+@pytest.mark.parametrize("name", list(SKEWED))
+def test_rank_skewed_marginals_stay_on_cluster_path(ctx, orc, name):
+    """Raw (non-uniform) marginals overflow the value-linear owner split; the
+    cluster kernel re-splits by exact quantile knots instead of handing the
+    block to the global path. Ranks stay bit-exact."""
+    rng = np.random.default_rng(hash(name) % 2**32)
+    n, k = 500000, 4  # 125k-row blocks: 9-CTA clusters in tail mode
+    f = SKEWED[name]
+    c1, c2 = f(rng.uniform(size=n)), f(rng.uniform(size=n))
+    off = np.linspace(0, n, k + 1).astype(np.uint64)
+    U = pcb.normalized_ranks(pcb.DataMatrix(c1, c2), off, ctx=ctx)
+    assert np.array_equal(U.u1, oracle_ranks(orc, c1, off))
+    assert np.array_equal(U.u2, oracle_ranks(orc, c2, off))
+    assert ctx.rank_paths() == {"cluster": 2 * k, "global": 0, "constant": 0, "invalid": 0}
+
+
+def test_rank_extreme_magnitudes_bit_exact(ctx, orc):
+    """Quantile-knot positions over keys spanning subnormals, signed zeros and
+    +-1e308 (halved-value interpolation, underflowed interval widths)."""
+    rng = np.random.default_rng(99)
+    n, k = 250000, 2
+    q = n // 8
+    tiny = rng.choice([-1.0, 1.0], q) * 5e-324 * rng.integers(1, 1 << 40, q)  # subnormals, few ties
+    parts = [rng.standard_normal(n - 2 * q - 64), rng.choice([-1.0, 1.0], q) * 10.0 ** rng.uniform(200, 308, q),
+             tiny, np.where(rng.random(64) < 0.5, -0.0, 0.0)]
+    c1 = np.concatenate(parts)
+    rng.shuffle(c1)
+    c2 = c1[::-1].copy()
+    off = np.linspace(0, n, k + 1).astype(np.uint64)
+    U = pcb.normalized_ranks(pcb.DataMatrix(c1, c2), off, ctx=ctx)
+    assert np.array_equal(U.u1, oracle_ranks(orc, c1, off))
+    assert np.array_equal(U.u2, oracle_ranks(orc, c2, off))
+    assert ctx.rank_paths()["cluster"] == 2 * k  # the quantile-knot split handled it
 
 
 def test_rank_forced_global_path_identical(ctx, env):
