@@ -573,7 +573,7 @@ __device__ void block_scan_excl_u16(uint32_t* cw, uint16_t* start, uint32_t n, u
 // array — the local sort keeps (bucket, index) in registers and the ranking
 // recomputes the bucket from the key; results are staged in the receive
 // buffer once the ranking is done — so a CTA needs 10 B per slot.
-template <int CTT, bool LEAN>
+template <int CTT, bool LEAN, bool QUANT = false>
 __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const ClusterJob* jobs, const double* c0, const double* c1,
                                                        uint64_t n_rows, unsigned long long* rp, uint32_t* route,
                                                        uint32_t* r2s_g, uint16_t* posl_g, uint32_t* ocnt, uint32_t K,
@@ -749,11 +749,12 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     }
 
     // ---- 2. per-warp counts of what this CTA sends to each value-range owner.
-    // Pass 0 splits [min, max] value-linearly (balanced for uniform-like data,
-    // e.g. pseudo-observations). If an owner would overflow its receive buffer
-    // (skewed raw marginals: normal, exponential, heavy tails), full CTAs in
-    // tail mode re-split by exact quantile knots and count again (pass 1);
-    // only if that still overflows does the block take the global path.
+    // The split is value-linear over [min, max] (balanced for uniform-like
+    // data, e.g. pseudo-observations). If an owner would overflow its receive
+    // buffer (skewed raw marginals: normal, exponential, heavy tails), the
+    // block is relaunched (fb 4) through the QUANT variant, which splits by
+    // exact quantile knots; only if that still overflows does the block take
+    // the global path.
     auto kclamp = [&](unsigned long long k) { return k < s_gmin ? s_gmin : (k > s_gmax ? s_gmax : k); };
     constexpr uint32_t NKMAX = 512;  // quantile knots (sample + exact extremes), < NKMAX used
     constexpr uint32_t SUBK = 128;   // an owner's share of the knot table (< SUBK - 1 intervals)
@@ -768,7 +769,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     constexpr uint32_t QTAB = 3200;
     __shared__ uint32_t s_ilo[kMaxCluster], s_ihi[kMaxCluster], s_qbad;
     __shared__ double s_qs;  // nbtot / N
-    bool qmode = false;
+    constexpr bool qmode = QUANT;
     unsigned long long* const knot = recv_key + 1536;
     uint32_t* const cum = reinterpret_cast<uint32_t*>(recv_key + 2336);
     double* const slope = reinterpret_cast<double*>(recv_key + 2600);
@@ -778,78 +779,10 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     uint16_t* const ivs = reinterpret_cast<uint16_t*>(recv_key + QTAB);  // interval id per slice element
     uint32_t bk[EMAX / 8];  // owner (4 bits) per element
     wait_slice();  // the mbarrier was initialised before the first __syncthreads
-    for (int pass = 0; pass < 2; ++pass) {
-#pragma unroll
-        for (int k = 0; k < EMAX / 8; ++k) bk[k] = 0u;
-        bool fin = true;
-#pragma unroll
-        for (int k = 0; k < EMAX; ++k) {
-            const uint32_t i = a + k * CTT + tid;
-            if (i < e) {
-                const double v = xs[i];
-                fin &= isfinite(v);
-                const unsigned long long kk = order_key(v);
-                const uint32_t d = (qmode ? qbucket(qpos(kk, ivs[i - a], knot, cum, slope), s_qs, nbtot)
-                                          : cbucket(kk, hm, scale, nbtot)) >> lg_nbl;
-                bk[k >> 3] |= d << ((k & 7) * 4);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < EMAX; ++k)  // the counts after all the (independent) owner lookups
-            if (a + k * CTT + tid < e) atomicAdd(&s_wc[wid][(bk[k >> 3] >> ((k & 7) * 4)) & 0xfu], 1u);
-        if (!__syncthreads_and(fin) && tid == 0) s_bad = 1;  // validate_data (pseudo_obs.hpp:34-36)
-        if (tid < CL) {  // totals per owner, and per-warp exclusive bases
-            uint32_t run = 0;
-            for (int w = 0; w < (CTT / 32); ++w) {
-                const uint32_t c = s_wc[w][tid];
-                s_wc[w][tid] = run;
-                run += c;
-            }
-            s_cnt[tid] = run;
-        }
-        cluster.sync();
-        mark(1);
-        if (tid < CL * CL) s_mat[tid] = *cluster.map_shared_rank(&s_cnt[tid % CL], tid / CL);  // [src][dst]
-        if (wid == 1) {
-            const int gb = __any_sync(0xffffffffu, lane < CL && *cluster.map_shared_rank(&s_bad, lane) != 0);
-            if (lane == 0) s_gbad = gb;
-        }
-        __syncthreads();
-        if (s_gbad) {
-            if (r == 0 && tid == 0) {
-                bad[J.seg] = 1;
-                fb[jid] = 2;
-            }
-            cluster.sync();
-            return;
-        }
-        const uint32_t cap = qmode ? RCAP - SUBSLOTS : RCAP;
-        if (wid == 0) {  // lane d: owner d's receive total and this CTA's offset in it
-            uint32_t col = 0, mine = 0;
-            if (lane < CL)
-                for (int q = 0; q < CL; ++q) {
-                    const uint32_t v = s_mat[q * CL + lane];
-                    col += v;
-                    if (q < r) mine += v;
-                }
-            if (lane < CL) s_off[lane] = mine;
-            const bool over = __any_sync(0xffffffffu, lane < CL && col > cap);
-            uint32_t below = lane < r ? col : 0u;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
-            const uint32_t total = __shfl_sync(0xffffffffu, col, r);
-            if (lane == 0) {
-                s_total = total;
-                s_base = below;
-                s_over = over;
-            }
-        }
-        __syncthreads();
-        if (!s_over) break;
-        if (LEAN || !tail || pass == 1 || RCAP < QTAB + (S + 3) / 4 + SUBSLOTS) {  // the global path takes the block
+    if constexpr (QUANT) {  // relaunch of the blocks the value-linear split could not balance
+        if (!tail || RCAP < QTAB + (S + 3) / 4 + SUBSLOTS) {  // no room for the tables: global path
             if (r == 0 && tid == 0) fb[jid] = 1;
             cluster.sync();
-            mark(2);
             return;
         }
         // ---- skewed block: equal-count owners from quantile knots. Knots =
@@ -877,7 +810,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         }
         if (tid == 0) s_qbad = 0;
         cta_extremes();  // exact slice extremes -> s_rmin/s_rmax
-        cluster.sync();  // samples and extremes visible; every peer is done with the first matrix
+        cluster.sync();  // samples and exact extremes visible
         cluster_extremes();
         const uint32_t ns = m * CL, nk = ns + 2;
         unsigned long long* const raw = recv_key + 512;
@@ -913,13 +846,13 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         for (uint32_t i0 = a + tid; i0 < e; i0 += 8 * CTT) {  // this slice's count per interval
             unsigned long long kk[8];
             uint32_t iv[8];
-#pragma unroll
+    #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const uint32_t i = i0 + u * CTT;
                 kk[u] = i < e ? order_key(xs[i]) : 0ull;
             }
             qsearch<9>(knot, kk, iv);
-#pragma unroll
+    #pragma unroll
             for (int u = 0; u < 8; ++u)
                 if (i0 + u * CTT < e) {
                     ivs[i0 + u * CTT - a] = static_cast<uint16_t>(iv[u]);
@@ -934,7 +867,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
             if (static_cast<uint32_t>(tid) < nk)
                 for (int q = 0; q < CL; ++q) c += *cluster.map_shared_rank(hc + tid, q);
             uint32_t x2 = c;
-#pragma unroll
+    #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, x2, o);
                 if (lane >= o) x2 += y;
@@ -943,7 +876,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
             __syncthreads();
             if (wid == 0) {
                 uint32_t z = lane < (CTT / 32) ? s_w[lane] : 0u;
-#pragma unroll
+    #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
                     if (lane >= o) z += y;
@@ -996,8 +929,80 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         }
         for (int q = tid; q < (CTT / 32) * kMaxCluster; q += CTT) (&s_wc[0][0])[q] = 0u;
         __syncthreads();
-        qmode = true;
         mark(7);
+    }
+#pragma unroll
+    for (int k = 0; k < EMAX / 8; ++k) bk[k] = 0u;
+    bool fin = true;
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k) {
+        const uint32_t i = a + k * CTT + tid;
+        if (i < e) {
+            const double v = xs[i];
+            fin &= isfinite(v);
+            const unsigned long long kk = order_key(v);
+            const uint32_t d = (qmode ? qbucket(qpos(kk, ivs[i - a], knot, cum, slope), s_qs, nbtot)
+                                      : cbucket(kk, hm, scale, nbtot)) >> lg_nbl;
+            bk[k >> 3] |= d << ((k & 7) * 4);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k)  // the counts after all the (independent) owner lookups
+        if (a + k * CTT + tid < e) atomicAdd(&s_wc[wid][(bk[k >> 3] >> ((k & 7) * 4)) & 0xfu], 1u);
+    if (!__syncthreads_and(fin) && tid == 0) s_bad = 1;  // validate_data (pseudo_obs.hpp:34-36)
+    if (tid < CL) {  // totals per owner, and per-warp exclusive bases
+        uint32_t run = 0;
+        for (int w = 0; w < (CTT / 32); ++w) {
+            const uint32_t c = s_wc[w][tid];
+            s_wc[w][tid] = run;
+            run += c;
+        }
+        s_cnt[tid] = run;
+    }
+    cluster.sync();
+    mark(1);
+    if (tid < CL * CL) s_mat[tid] = *cluster.map_shared_rank(&s_cnt[tid % CL], tid / CL);  // [src][dst]
+    if (wid == 1) {
+        const int gb = __any_sync(0xffffffffu, lane < CL && *cluster.map_shared_rank(&s_bad, lane) != 0);
+        if (lane == 0) s_gbad = gb;
+    }
+    __syncthreads();
+    if (s_gbad) {
+        if (r == 0 && tid == 0) {
+            bad[J.seg] = 1;
+            fb[jid] = 2;
+        }
+        cluster.sync();
+        return;
+    }
+    const uint32_t cap = qmode ? RCAP - SUBSLOTS : RCAP;
+    if (wid == 0) {  // lane d: owner d's receive total and this CTA's offset in it
+        uint32_t col = 0, mine = 0;
+        if (lane < CL)
+            for (int q = 0; q < CL; ++q) {
+                const uint32_t v = s_mat[q * CL + lane];
+                col += v;
+                if (q < r) mine += v;
+            }
+        if (lane < CL) s_off[lane] = mine;
+        const bool over = __any_sync(0xffffffffu, lane < CL && col > cap);
+        uint32_t below = lane < r ? col : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+        const uint32_t total = __shfl_sync(0xffffffffu, col, r);
+        if (lane == 0) {
+            s_total = total;
+            s_base = below;
+            s_over = over;
+        }
+    }
+    __syncthreads();
+    if (s_over) {  // QUANT kernel: the global path takes the block; otherwise the quantile relaunch if it fits
+        if (r == 0 && tid == 0)
+            fb[jid] = (!QUANT && !LEAN && tail && RCAP >= QTAB + (S + 3) / 4 + SUBSLOTS) ? 4 : 1;
+        cluster.sync();
+        mark(2);
+        return;
     }
     for (int q = tid; q < (CTT / 32) * CL; q += CTT) s_wc[q / CL][q % CL] += s_off[q % CL];
     __syncthreads();
@@ -1153,9 +1158,13 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     mark(5);
 }
 
-void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, uint32_t njobs, const double* c0,
-                         const double* c1, uint64_t n_rows, RankOut& out, int32_t* fb, int32_t* bad) {
-    auto kern = p.lean ? k_rank_cluster_t<kLeanT, true> : k_rank_cluster_t<CT, false>;
+// quant: the quantile-knot variant, for the jobs the value-linear split could
+// not balance (fb 4 from the first launch); K = blocks (output indexing)
+void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, uint32_t njobs, uint32_t K,
+                         const double* c0, const double* c1, uint64_t n_rows, RankOut& out, int32_t* fb,
+                         int32_t* bad, bool quant = false) {
+    auto kern = p.lean ? k_rank_cluster_t<kLeanT, true>
+                       : (quant ? k_rank_cluster_t<CT, false, true> : k_rank_cluster_t<CT, false>);
     // tail mode when the slice fits after the receive buffer (full CTAs only)
     cudaFuncAttributes fa;
     PCB_CUDA(cudaFuncGetAttributes(&fa, kern));
@@ -1186,15 +1195,15 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
     }
     PCB_CUDA(cudaLaunchKernelEx(&cfg, kern, jobs, c0, c1, n_rows, out.rp, out.route, out.r2s, out.posl,
                                 out.ocnt,
-                                njobs / 2, fb, bad, p.cl, p.rcap, p.lg_nbl, tail, prof));
+                                K, fb, bad, p.cl, p.rcap, p.lg_nbl, tail, prof));
     if (prof) {
         unsigned long long h[12];
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
         PCB_CUDA(cudaStreamSynchronize(c.stream));
         const double ctas = static_cast<double>(njobs) * p.cl;
-        std::fprintf(stderr, "[rank profile] CL=%d S=%u lean=%d: cycles/CTA  minmax %.0f  count %.0f  matrix %.0f  "
+        std::fprintf(stderr, "[rank profile%s] CL=%d S=%u lean=%d: cycles/CTA  minmax %.0f  count %.0f  matrix %.0f  "
                      "send %.0f  localsort %.0f  rank %.0f  qsample+sort %.0f  qhist-loop %.0f  qhist-sync %.0f  qcum %.0f  "
-                     "qshare %.0f\n", p.cl, p.s, int(p.lean), h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
+                     "qshare %.0f\n", quant ? " quantile" : "", p.cl, p.s, int(p.lean), h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
                      h[4] / ctas, h[5] / ctas, h[6] / ctas, h[8] / ctas, h[9] / ctas, h[10] / ctas, h[7] / ctas);
     }
     c.count_launch();
@@ -1435,10 +1444,29 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
         out.r2s = c.ws.get_t<uint32_t>("rank.r2s", nslot);
         out.posl = c.ws.get_t<uint16_t>("rank.posl", nslot);
         out.ocnt = c.ws.get_t<uint32_t>("rank.ocnt", static_cast<size_t>(njobs) * plan.cl);
-        launch_rank_cluster(c, plan, jobs, njobs, d_col1, d_col2, n_rows, out, fb, d_bad);
+        launch_rank_cluster(c, plan, jobs, njobs, static_cast<uint32_t>(K), d_col1, d_col2, n_rows, out, fb, d_bad);
         std::vector<int32_t> hfb(njobs);
         PCB_CUDA(cudaMemcpyAsync(hfb.data(), fb, njobs * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
         PCB_CUDA(cudaStreamSynchronize(c.stream));
+        // skewed blocks (fb 4): relaunch them through the quantile-knot variant
+        std::vector<uint32_t> skew;
+        for (uint32_t j = 0; j < njobs; ++j)
+            if (hfb[j] == 4) skew.push_back(j);
+        if (!skew.empty()) {
+            const uint32_t nq = static_cast<uint32_t>(skew.size());
+            auto* qjobs = c.ws.get_t<ClusterJob>("rank.qjobs", nq);
+            auto* qfb = c.ws.get_t<int32_t>("rank.qfb", nq);
+            std::vector<ClusterJob> hq(nq);
+            for (uint32_t i = 0; i < nq; ++i) hq[i] = hj[skew[i]];
+            PCB_CUDA(cudaMemcpyAsync(qjobs, hq.data(), nq * sizeof(ClusterJob), cudaMemcpyHostToDevice, c.stream));
+            PCB_CUDA(cudaMemsetAsync(qfb, 0, nq * sizeof(int32_t), c.stream));
+            launch_rank_cluster(c, plan, qjobs, nq, static_cast<uint32_t>(K), d_col1, d_col2, n_rows, out, qfb, d_bad,
+                                true);
+            std::vector<int32_t> hqfb(nq);
+            PCB_CUDA(cudaMemcpyAsync(hqfb.data(), qfb, nq * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+            PCB_CUDA(cudaStreamSynchronize(c.stream));
+            for (uint32_t i = 0; i < nq; ++i) hfb[skew[i]] = hqfb[i];
+        }
         // a block is routed when both columns went through the cluster path;
         // cluster-ranked columns of other blocks get their by-row ranks rebuilt
         const bool force_rows = getenv_flag("PCB_VAR_GLOBAL");
