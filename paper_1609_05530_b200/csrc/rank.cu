@@ -1121,16 +1121,16 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         const unsigned long long kv = recv_key[j];
         const uint32_t lb = LEAN ? (cbucket(kv, hm, scale, nbtot) & lmask) : (outw[j] & 0x3fffu);
         const uint32_t s0 = lhs[lb], s1 = lhs[lb + 1];
-        uint32_t less = 0, same = 0, before = 0;
-#pragma unroll 1
+        uint32_t less = 0, sb = 0;  // sb = same | before << 16 (both < 2^14): one accumulator, no moves
+#pragma unroll 2
         for (uint32_t q = s0; q < s1; ++q) {
             const uint32_t o = perm[q];
             const unsigned long long kq = recv_key[o];
             less += kq < kv;
-            const bool eqk = kq == kv;
-            same += eqk;
-            before += eqk && o < j;
+            const uint32_t eq = kq == kv;
+            sb += eq + ((eq & static_cast<uint32_t>(o < j)) << 16);
         }
+        const uint32_t same = sb & 0xffffu, before = sb >> 16;
         const uint32_t llt = s0 + less;  // < T <= 16384, so local r2 = 2*llt + same + 1 <= 2T < 2^16
         const uint32_t res = ((2u * llt + same + 1u) << 16) | (llt + before) | (before == 0 ? 0x8000u : 0u);
         // full CTAs: outw[j] (this element's bucket) is read only by this thread,
