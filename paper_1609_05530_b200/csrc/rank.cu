@@ -523,9 +523,15 @@ __device__ __forceinline__ uint32_t qbucket(double g, double qs, uint32_t nbtot)
     return min(nbtot - 1u, static_cast<uint32_t>(__dmul_rn(g, qs)));
 }
 
+// value-linear global bucket, clamped at both ends (the conversion saturates
+// below 0 and maps NaN to 0); monotone in the value. Senders bucket the value
+// itself, owners the received key: key_value(order_key(v)) is v (+0 for -0,
+// the same t), so both agree bit for bit.
+__device__ __forceinline__ uint32_t cbucket_v(double v, double hm, double scale, uint32_t nbtot) {
+    return min(__double2uint_rz((0.5 * v - hm) * scale), nbtot - 1u);
+}
 __device__ __forceinline__ uint32_t cbucket(unsigned long long k, double hm, double scale, uint32_t nbtot) {
-    const double t = (0.5 * key_value(k) - hm) * scale;  // monotone in k; clamped at both ends
-    return t > 0.0 ? (t < static_cast<double>(nbtot) ? static_cast<uint32_t>(t) : nbtot - 1u) : 0u;
+    return cbucket_v(key_value(k), hm, scale, nbtot);
 }
 
 // Same scan over NBL u16 counters packed two per word (`cw`); writes the u16
@@ -940,9 +946,8 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         if (i < e) {
             const double v = xs[i];
             fin &= isfinite(v);
-            const unsigned long long kk = order_key(v);
-            const uint32_t d = (qmode ? qbucket(qpos(kk, ivs[i - a], knot, cum, slope), s_qs, nbtot)
-                                      : cbucket(kk, hm, scale, nbtot)) >> lg_nbl;
+            const uint32_t d = (qmode ? qbucket(qpos(order_key(v), ivs[i - a], knot, cum, slope), s_qs, nbtot)
+                                      : cbucket_v(v, hm, scale, nbtot)) >> lg_nbl;
             bk[k >> 3] |= d << ((k & 7) * 4);
         }
     }
@@ -1121,7 +1126,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         const unsigned long long kv = recv_key[j];
         const uint32_t lb = LEAN ? (cbucket(kv, hm, scale, nbtot) & lmask) : (outw[j] & 0x3fffu);
         const uint32_t s0 = lhs[lb], s1 = lhs[lb + 1];
-        uint32_t less = 0, sb = 0;  // sb = same | before << 16 (both < 2^14): one accumulator, no moves
+        uint32_t less = 0, sb = 0;  // sb = same | before << 16 (both <= 2^14): one accumulator, no moves
 #pragma unroll 2
         for (uint32_t q = s0; q < s1; ++q) {
             const uint32_t o = perm[q];
