@@ -483,6 +483,14 @@ inline ClusterPlan plan_cluster(uint64_t nmax) {
     return ClusterPlan{};
 }
 
+// 8-byte store into CTA `rank`'s shared memory at this CTA's shared address
+// `saddr` (mapa + st.shared::cluster: 32-bit addressing, no generic window)
+__device__ __forceinline__ void dsmem_st64(uint32_t saddr, uint32_t rank, unsigned long long v) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(saddr), "r"(rank));
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(ra), "l"(v) : "memory");
+}
+
 // Quantile-knot map for skewed blocks (the cluster kernel's second pass):
 // kn[0..nk) sorted knot keys with kn[0] <= k, cm[j] = elements before
 // interval j (exact, cluster-wide). Interval i = [kn[i], kn[i+1]); the last
@@ -1016,6 +1024,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     // The owner never needs the row: its outputs are written per receive slot
     // and the row finds them through route[row] = (owner, slot).
     constexpr int SB = 8;  // slice reloads in flight per thread (L2 hits)
+    const uint32_t recv_sa = static_cast<uint32_t>(__cvta_generic_to_shared(recv_key));
     if (tail) {
 #pragma unroll
       for (int k = 0; k < EMAX; ++k) {
@@ -1025,7 +1034,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
             const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
             const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
             route[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = (d << 16) | slot;
-            *cluster.map_shared_rank(recv_key + slot, d) = kk;
+            dsmem_st64(recv_sa + slot * 8u, d, kk);
         }
       }
     } else
@@ -1047,7 +1056,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
             const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
             const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
             route[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = (d << 16) | slot;
-            *cluster.map_shared_rank(recv_key + slot, d) = kk;
+            dsmem_st64(recv_sa + slot * 8u, d, kk);
         }
       }
     }
