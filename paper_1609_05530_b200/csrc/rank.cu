@@ -410,7 +410,6 @@ uint32_t tiles_of(uint64_t n) { return static_cast<uint32_t>((n + RTILE - 1) / R
 // skewed data) or
 // a non-finite range falls back to the global path.
 constexpr int CT = 1024;  // threads per cluster CTA
-constexpr int NWARP = CT / 32;
 constexpr int EMAX = 16;         // slice elements per thread (slice <= 16K)
 constexpr int QMAX = 16;         // received elements per thread (RCAP <= QMAX * CT)
 constexpr int kMaxCluster = 16;

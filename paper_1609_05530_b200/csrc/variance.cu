@@ -42,7 +42,6 @@ namespace {
 namespace cg = cooperative_groups;
 
 constexpr int VT = 1024;  // threads per cluster CTA
-constexpr int VNW = VT / 32;
 
 // Per-theta constants, built once per CTA (they cost more than a point).
 template <int FAM>
