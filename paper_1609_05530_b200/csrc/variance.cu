@@ -41,7 +41,6 @@ namespace {
 
 namespace cg = cooperative_groups;
 
-constexpr int VT = 1024;  // threads per cluster CTA
 
 // Per-theta constants, built once per CTA (they cost more than a point).
 template <int FAM>
