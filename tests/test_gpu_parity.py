@@ -319,6 +319,22 @@ def test_rank_skewed_marginals_stay_on_cluster_path(ctx, orc, name):
     assert ctx.rank_paths() == {"cluster": 2 * k, "global": 0, "constant": 0, "invalid": 0}
 
 
+@pytest.mark.parametrize("fam,theta,name", [(1, 5.0, "normal"), (2, 2.0, "cauchy"), (0, 0.5, "lognormal")])
+def test_fit_on_skewed_raw_marginals(ctx, orc, fam, theta, name):
+    """Raw columns with skewed marginals (quantile-split ranks in slot space)
+    through the whole pipeline: theta-hat, sigma2 and the combine against the
+    oracle on the same bytes."""
+    n, k = 1_000_000, 8  # 125k-row blocks
+    X = pcb.sample_matrix(fam, theta, n, k, ctx=ctx)
+    f = SKEWED[name]
+    c1, c2 = f(np.asarray(X.col1)), f(np.asarray(X.col2))
+    off = orc.partition(n, k)
+    got = pcb.fit_blocks(fam, pcb.DataMatrix(c1, c2), off, ctx=ctx)
+    assert ctx.rank_paths()["global"] == 0
+    want = orc.fit_blocks(fam, c1, c2, off)
+    check_records(got, want, TOL64)
+
+
 def test_rank_extreme_magnitudes_bit_exact(ctx, orc):
     """Quantile-knot positions over keys spanning subnormals, signed zeros and
     +-1e308 (halved-value interpolation, underflowed interval widths)."""
