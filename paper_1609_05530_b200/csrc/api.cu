@@ -193,6 +193,23 @@ void pipeline_blocks_host(pcb::Ctx& c, int fam, int prec, const double* h1, cons
         groups.push_back({b0, b1});
         b0 = b1;
     }
+    // the last group's compute is the only part no copy hides: split it into
+    // halving pieces (1/2, 1/4, ... down to ~target/8) so the exposed tail is small
+    if (groups.size() > 1) {
+        const auto last = groups.back();
+        groups.pop_back();
+        uint64_t b0 = last.first;
+        while (b0 < last.second) {
+            const uint64_t rest = off[last.second] - off[b0];
+            uint64_t b1 = last.second;
+            if (rest > target / 8) {  // take about half of what is left, in whole blocks
+                b1 = b0 + 1;
+                while (b1 < last.second && off[b1 + 1] - off[b0] <= rest / 2) ++b1;
+            }
+            groups.push_back({b0, b1});
+            b0 = b1;
+        }
+    }
     if (groups.size() == 1) {
         const double* d1 = dev_in(c, h1, n_rows, "c1");
         const double* d2 = dev_in(c, h2, n_rows, "c2");
