@@ -193,7 +193,10 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
 #ifndef PCB_U_PREP
 #define PCB_U_PREP 4
 #endif
-    constexpr int U = FAM == kGumbel ? 2 : PCB_U_PREP;  // points per thread in flight (measured at C5)
+#ifndef PCB_U_PREP_U
+#define PCB_U_PREP_U 2
+#endif
+    constexpr int U = FAM == kGumbel ? PCB_U_PREP_U : PCB_U_PREP;  // points per thread in flight (measured at C5)
     for (int k0 = 0; k0 < PPT; k0 += U) {
         double uu[U], ww[U], gx[U], gy[U];
         uint32_t ra[U], rb[U];
