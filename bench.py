@@ -292,31 +292,44 @@ def run_ours(args):
             traffic_db = json.load(open(tp))
         except Exception:
             traffic_db = {}
+    # L2: sectors per point per kernel and family (ncu, profiles/l2_sectors.json) against the
+    # measured random-sector L2 rate (tools/l2_probe.cu, profiles/l2_probe.json): the bound of the
+    # gather kernels (prepare, variance passes), reported beside the HBM roofline
+    l2_db, l2_rate = {}, None
+    try:
+        l2_db = json.load(open(os.path.join(ROOT, "profiles", "l2_sectors.json")))
+        l2_rate = float(json.load(open(os.path.join(ROOT, "profiles", "l2_probe.json")))["l2_random_sectors_per_s"])
+    except Exception:
+        l2_db, l2_rate = {}, None
+    l2_sect = {}  # kernel -> sectors per step
     per_kernel = {}  # name -> [ms, launches, bytes, fp64 instr]
-    def add(name, ms, launches, nbytes, instr):
+    def add(name, ms, launches, nbytes, instr, fam_name, per_launch=False):
         e = per_kernel.setdefault(name, [0.0, 0, 0.0, 0.0])
         e[0] += ms
         e[1] += launches
         e[2] += nbytes
         e[3] += instr
+        spp = l2_db.get(name, {}).get(fam_name) if isinstance(l2_db.get(name), dict) else None
+        if spp is not None and ms > 0:
+            l2_sect[name] = l2_sect.get(name, 0.0) + spp * rows * (launches if per_launch else 1)
     for name, fam, th in FAMILIES:
         st_ = kernels[name]["stage_ms"]
-        add("k_rank_cluster", st_.get("rank", 0.0), 1, 32.0 * rows, 0.0)
+        add("k_rank_cluster", st_.get("rank", 0.0), 1, 32.0 * rows, 0.0, name)
         # prepare: read 2 packed ranks; write T (f64 pair) + its fp32 warm-up copy (Archimedean)
-        add("k_prepare", st_.get("prepare", 0.0), 1, (16.0 if name == "gaussian" else 40.0) * rows, 0.0)
+        add("k_prepare", st_.get("prepare", 0.0), 1, (16.0 if name == "gaussian" else 40.0) * rows, 0.0, name)
         vp = st_.get("var_point_ms", 0.0)
         # variance pass 1: read ranks + routes (+T for Gumbel); write score + two routed cross values
-        add("k_var_point", vp, 1, (64.0 if name == "gumbel" else 48.0) * rows, F_VAR[name] * rows)
+        add("k_var_point", vp, 1, (64.0 if name == "gumbel" else 48.0) * rows, F_VAR[name] * rows, name)
         # passes 2-3: scan reads cross + local position, writes W per slot (2 x 18 B);
         # final reads route, score, W_1, W_2 (32 B)
-        add("k_var_scan+final", st_.get("variance", 0.0) - vp, 2, 68.0 * rows, 0.0)
+        add("k_var_scan+final", st_.get("variance", 0.0) - vp, 2, 68.0 * rows, 0.0, name)
         if "lik" in kernels[name]:
             lk = kernels[name]["lik"]
             add("k_lik(fp64)", lk["ms"], lk["launches"], B_PASS * rows * lk["fp64_passes"],
-                F_FIT[name] * rows * lk["fp64_passes"])
+                F_FIT[name] * rows * lk["fp64_passes"], name, per_launch=True)
         if "warm_fp32" in kernels[name]:
             wk = kernels[name]["warm_fp32"]
-            add("k_lik(fp32 warm-up)", wk["ms"], wk["launches"], 8.0 * rows * wk["launches"], 0.0)
+            add("k_lik(fp32 warm-up)", wk["ms"], wk["launches"], 8.0 * rows * wk["launches"], 0.0, name, per_launch=True)
     table = {}
     for kname, (kms, nl, nbytes, instr) in per_kernel.items():
         if kms <= 0:
@@ -329,6 +342,10 @@ def run_ours(args):
             ach, peak, unit = instr / (kms * 1e-3) / 1e12, fp64_peak / 1e12, "T FP64-instr/s"
         table[kname] = {"ms_per_step": kms, "share": kms / ms, "launches": nl, "bound": bound, "achieved": ach,
                         "peak": peak, "unit": unit, "frac": ach / peak, "avg_launch_ms": kms / max(nl, 1)}
+        if kname in l2_sect and l2_rate:
+            rate = l2_sect[kname] / (kms * 1e-3)
+            table[kname]["l2"] = {"sectors_per_s": rate, "peak_random_sectors_per_s": l2_rate,
+                                  "frac": rate / l2_rate, "source": "profiles/l2_sectors.json x live ms"}
     dom = max(table, key=lambda k: table[k]["ms_per_step"]) if table else None
     roof = None
     if dom:
