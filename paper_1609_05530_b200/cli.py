@@ -4,6 +4,7 @@
     python -m paper_1609_05530_b200.cli split-fit FILE.csv --family frank --subsets 10 [--scheme strided] [--out blocks.csv]
     python -m paper_1609_05530_b200.cli simulate --family gumbel --theta 2 --rows 50000 --subsets 10 \\
         --replicates 5 --seed 0x160905530 --out results/
+    python -m paper_1609_05530_b200.cli report results/ [--out report_dir]
 
 Exit codes: 0 success, 2 usage error, 3 data error, 4
 convergence failure. Output CSVs carry a versioned schema comment line.
@@ -130,6 +131,75 @@ def cmd_simulate(args) -> int:
     return 0
 
 
+SUMMARY_COLS = ["family", "theta_true", "N", "M", "S", "theta_full_sim", "theta_combined_sim", "bias", "mse",
+                "rel_l1", "rel_l2", "mean_subset_s", "mean_full_s", "seed"]
+FAMILY_NAMES = {0: "gaussian", 1: "frank", 2: "gumbel"}
+
+
+def cmd_report(args) -> int:  # merge summary.csv files into Table-1 layout + metric tables
+    found, rows = [], []
+    for root, _, files in sorted(os.walk(args.results)):
+        for fn in sorted(files):
+            if fn == "summary.csv":
+                found.append(os.path.join(root, fn))
+    for path in found:
+        try:
+            lines = open(path).read().splitlines()
+        except OSError as e:
+            print(f"error: {path}: {e}", file=sys.stderr)
+            continue
+        if not lines or lines[0].strip() != SCHEMA:
+            print(f"error: {path}: schema mismatch (expected '{SCHEMA}')", file=sys.stderr)
+            continue
+        rd = list(csv.DictReader(io.StringIO("\n".join(lines[1:]))))
+        if not rd or any(c not in rd[0] for c in SUMMARY_COLS):
+            print(f"error: {path}: missing columns", file=sys.stderr)
+            continue
+        for r in rd:
+            try:
+                rows.append({"family": FAMILY_NAMES.get(int(r["family"]), r["family"]), "theta": float(r["theta_true"]),
+                             "N": int(r["N"]), "M": int(r["M"]), "S": int(r["S"]), "bias": float(r["bias"]),
+                             "mse": float(r["mse"]), "rel_l1": float(r["rel_l1"]), "rel_l2": float(r["rel_l2"]),
+                             "sub_s": float(r["mean_subset_s"]), "full_s": float(r["mean_full_s"])})
+            except (KeyError, ValueError) as e:
+                print(f"error: {path}: corrupt row ({e})", file=sys.stderr)
+    if not rows:
+        print("error: data: no results found", file=sys.stderr)
+        return 3
+    out = args.out or args.results
+    os.makedirs(out, exist_ok=True)
+    # Table 1 layout (PAPER Table 1): per (family, N) the mean per-subset seconds for each M and full-data seconds
+    ms = sorted({r["M"] for r in rows})
+    cells = {}
+    for r in rows:
+        c = cells.setdefault((r["family"], r["N"]), {"sub": {}, "full": []})
+        c["sub"].setdefault(r["M"], []).append(r["sub_s"])
+        c["full"].append(r["full_s"])
+    order = {"gaussian": 0, "frank": 1, "gumbel": 2}
+    keys = sorted(cells, key=lambda k: (order.get(k[0], 9), k[1]))
+    timing = [["family", "N"] + [f"subset_s_M{m}" for m in ms] + ["full_s"]]
+    for fam, n in keys:
+        c = cells[(fam, n)]
+        timing.append([fam, str(n)] + [repr(float(np.mean(c["sub"][m]))) if m in c["sub"] else "" for m in ms]
+                      + [repr(float(np.mean(c["full"])))])
+    acc = [["family", "theta_true", "N", "M", "S", "bias", "mse", "rel_l1", "rel_l2"]]
+    for r in sorted(rows, key=lambda r: (order.get(r["family"], 9), r["theta"], r["N"], r["M"])):
+        acc.append([r["family"], repr(r["theta"]), str(r["N"]), str(r["M"]), str(r["S"]), repr(r["bias"]),
+                    repr(r["mse"]), repr(r["rel_l1"]), repr(r["rel_l2"])])
+    for name, table in (("report_timing.csv", timing), ("report_accuracy.csv", acc)):
+        with open(os.path.join(out, name), "w") as f:
+            f.write(SCHEMA + "\n" + "\n".join(",".join(t) for t in table) + "\n")
+    _manifest(out, "report", {"results": os.path.abspath(args.results), "files": found, "rows": len(rows),
+                              "time": time.time()})
+    for title, table in (("Computation time (seconds): mean per subset by M, full data", timing),
+                         ("Accuracy of the combined estimate", acc)):
+        w = [max(len(t[i]) for t in table) for i in range(len(table[0]))]
+        print(title)
+        for t in table:
+            print("  " + "  ".join(x.rjust(w[i]) for i, x in enumerate(t)))
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="parcop-b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -151,10 +221,15 @@ def main(argv=None) -> int:
     p.add_argument("--quad-nodes", type=int, default=200)
     p.add_argument("--seed", default=hex(0x160905530))
     p.add_argument("--out", default="results")
+    p = sub.add_parser("report")
+    p.add_argument("results")
+    p.add_argument("--out", default=None)
     try:
         args = ap.parse_args(argv)
     except SystemExit as e:
         return 2 if e.code else 0
+    if args.cmd == "report":  # host-only: reads CSVs, no device needed
+        return cmd_report(args)
     import paper_1609_05530_b200 as pcb
     try:
         return {"fit": cmd_fit, "split-fit": cmd_split_fit, "simulate": cmd_simulate}[args.cmd](args)

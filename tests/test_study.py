@@ -66,6 +66,33 @@ def test_cli_data_and_usage_errors(tmp_path):
     assert len(c1) == 100 and c2[3] == 0.5 * 3
 
 
+def _summary(path, rows):
+    path.parent.mkdir(parents=True, exist_ok=True)
+    head = ",".join(cli.SUMMARY_COLS)
+    path.write_text(cli.SCHEMA + "\n" + head + "\n" + "\n".join(",".join(str(x) for x in r) for r in rows) + "\n")
+
+
+def test_cli_report(tmp_path, capsys):
+    empty = tmp_path / "empty"
+    empty.mkdir()
+    assert cli.main(["report", str(empty)]) == 3  # "no results found"
+    res = tmp_path / "results"
+    _summary(res / "g" / "summary.csv", [[0, 0.3, 50000, 10, 5, 0.3, 0.301, 0.001, 2e-6, 0.01, 0.012, 0.5, 20.0, 1],
+                                         [0, 0.3, 50000, 100, 5, 0.3, 0.302, 0.002, 5e-6, 0.02, 0.03, 0.05, 21.0, 1]])
+    _summary(res / "f" / "summary.csv", [[1, 5.0, 50000, 10, 5, 5.0, 5.01, 0.01, 1e-4, 0.01, 0.02, 0.7, 30.0, 2]])
+    bad = res / "old" / "summary.csv"
+    bad.parent.mkdir(parents=True)
+    bad.write_text("# parcop-b200 csv schema v0\nfamily\n")
+    assert cli.main(["report", str(res), "--out", str(tmp_path / "rep")]) == 0
+    err = capsys.readouterr().err
+    assert "schema mismatch" in err
+    timing = (tmp_path / "rep" / "report_timing.csv").read_text().splitlines()
+    assert timing[0] == cli.SCHEMA and timing[1] == "family,N,subset_s_M10,subset_s_M100,full_s"
+    assert timing[2] == "gaussian,50000,0.5,0.05,20.5" and timing[3] == "frank,50000,0.7,,30.0"
+    acc = (tmp_path / "rep" / "report_accuracy.csv").read_text().splitlines()
+    assert len(acc) == 2 + 3 and acc[2].startswith("gaussian,0.3,50000,10,5,0.001,")
+
+
 def _write_pairs(path, header):
     lines = (["u,v"] if header else []) + [f"{i * 0.01!r},{0.5 * i!r}" for i in range(100)]
     path.write_text("\n".join(lines) + "\n")
