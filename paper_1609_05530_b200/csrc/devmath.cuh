@@ -195,24 +195,6 @@ __device__ __forceinline__ void frank_sh(double u, double v, const FrankTheta& f
     h = f.hconst - 2.0 * (bpp * rb - q * q);
 }
 
-#ifdef PCB_EXP_SCORE_ONLY
-__device__ __forceinline__ void frank_s(double u, double v, const FrankTheta& f, double& s) {
-    if (f.neg) v = 1.0 - v;
-    const double t = f.t;
-    const double lo = fmin(u, v), hi = fmax(u, v);
-    const double ema = expm1(-t * (1.0 - lo));
-    const double e2 = exp(-t * (hi - lo));
-    const double emb = expm1(-t * lo);
-    const double e1 = 1.0 + ema, e3 = 1.0 + emb;
-    const double b = ema + e2 * emb;
-    const double sum = lo + hi;
-    const double bp = lo - e1 + e2 * (hi - sum * e3);
-    const double q = bp * fast_rcp(b);
-    const double sc = f.inv_t - f.g - sum - 2.0 * q;
-    s = f.neg ? -sc : sc;
-}
-#endif
-
 // fp32 per-point arithmetic (likelihood path of configs[3]); the caller
 // accumulates in fp64.
 struct FrankThetaF {

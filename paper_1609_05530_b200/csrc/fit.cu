@@ -376,12 +376,7 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
                 if (i < cnt) {
                     const TI p = Tb[i];
                     double s, h;
-#ifdef PCB_EXP_SCORE_ONLY
-                    frank_s(p.x, p.y, f, s);
-                    h = -1.0;
-#else
                     frank_sh(p.x, p.y, f, s, h);
-#endif
                     v[0] += s;
                     v[1] += h;
                 }
