@@ -592,7 +592,8 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
                                                        uint32_t* r2s_g, uint16_t* posl_g, uint32_t* ocnt, uint32_t K,
                                                        int32_t* fb,
                                                        int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
-                                                       int tail, unsigned long long* prof) {
+                                                       int tail, unsigned long long* prof, uint32_t njobs,
+                                                       uint32_t pf) {
     namespace cg = cooperative_groups;
     constexpr int QM = LEAN ? 18 : QMAX;  // received elements per thread (RCAP <= QM * CTT)
     long long t_prev = clock64();
@@ -644,6 +645,20 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
                 static_cast<uint32_t>(__cvta_generic_to_shared(stage_at))),
             "l"(g_lo), "r"(bytes), "r"(mb)
             : "memory");
+    }
+    // the job pf positions ahead runs on the next wave of clusters: pull this
+    // CTA's slice of it into L2 now, so its staging copy and sample read L2
+    if (tid == 32 && pf && jid + pf < njobs) {
+        const ClusterJob J2 = jobs[jid + pf];
+        const uint32_t S2 = slice_of(J2.n, CL);
+        const uint32_t a2 = min(J2.n, r * S2), e2 = min(J2.n, a2 + S2);
+        if (e2 > a2) {
+            const double* x2 = (J2.col ? c1 : c0) + J2.begin;
+            const uint64_t p_lo = reinterpret_cast<uint64_t>(x2 + a2) & ~15ull;
+            const uint64_t p_hi = (reinterpret_cast<uint64_t>(x2 + e2) + 15ull) & ~15ull;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p_lo), "r"(static_cast<uint32_t>(p_hi - p_lo))
+                         : "memory");
+        }
     }
     auto wait_slice = [&]() {
         if (!staged) return;
@@ -1201,6 +1216,16 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // L2 prefetch distance (jobs): one wave of co-resident clusters ahead
+    uint32_t pf = 0;
+    if (const char* e = std::getenv("PCB_RANK_PF")) {
+        pf = static_cast<uint32_t>(std::atoi(e));
+    } else {
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void*>(kern), &cfg) == cudaSuccess && ncl > 0)
+            pf = static_cast<uint32_t>(ncl);
+        cudaGetLastError();
+    }
     unsigned long long* prof = nullptr;
     if (getenv_flag("PCB_RANK_PROFILE")) {
         prof = c.ws.get_t<unsigned long long>("rank.prof", 12);
@@ -1208,7 +1233,7 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
     }
     PCB_CUDA(cudaLaunchKernelEx(&cfg, kern, jobs, c0, c1, n_rows, out.rp, out.route, out.r2s, out.posl,
                                 out.ocnt,
-                                K, fb, bad, p.cl, p.rcap, p.lg_nbl, tail, prof));
+                                K, fb, bad, p.cl, p.rcap, p.lg_nbl, tail, prof, njobs, pf));
     if (prof) {
         unsigned long long h[12];
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));

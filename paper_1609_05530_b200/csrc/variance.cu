@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(ST, 1) k_var_scan(const BlockState* st, const 
                                                    const uint16_t* __restrict__ posl,
                                                    const uint32_t* __restrict__ ocnt, double* __restrict__ xr,
                                                    double* __restrict__ tot, int CL, uint32_t RCAP,
-                                                   unsigned long long* prof) {
+                                                   unsigned long long* prof, uint32_t pf) {
     long long t_prev = clock64();
     auto mark = [&](int k) {  // optional phase timing (PCB_VAR_PROFILE)
         if (prof && threadIdx.x == 0) {
@@ -308,6 +308,25 @@ __global__ void __launch_bounds__(ST, 1) k_var_scan(const BlockState* st, const 
         if (j < RCAP) {
             pv0[k] = P[j];
             x0[k] = X[j];
+        }
+    }
+    // the CTA pf positions ahead runs on the next wave (one CTA per SM): pull
+    // its slots into L2 while this CTA's scan keeps HBM otherwise idle
+    if (tid == 32 && pf && blockIdx.x + pf < gridDim.x) {
+        const uint32_t b2 = blockIdx.x + pf;
+        const int col2 = static_cast<int>(b2 / (njobs * CL));
+        const int rem2 = static_cast<int>(b2 - col2 * njobs * CL);
+        const uint64_t rid2 = (static_cast<uint64_t>(col2) * nseg + seg_list[rem2 / CL]) * CL + rem2 % CL;
+        const uint32_t T2 = ocnt[rid2];
+        if (T2) {
+            const uint64_t xlo = reinterpret_cast<uint64_t>(xr + rid2 * RCAP) & ~15ull;
+            const uint64_t xhi = (reinterpret_cast<uint64_t>(xr + rid2 * RCAP + T2) + 15ull) & ~15ull;
+            const uint64_t plo = reinterpret_cast<uint64_t>(posl + rid2 * RCAP) & ~15ull;
+            const uint64_t phi = (reinterpret_cast<uint64_t>(posl + rid2 * RCAP + T2) + 15ull) & ~15ull;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xlo), "r"(static_cast<uint32_t>(xhi - xlo))
+                         : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(plo), "r"(static_cast<uint32_t>(phi - plo))
+                         : "memory");
         }
     }
     if (st[m].status != kConverged) return;
@@ -615,7 +634,16 @@ void launch_var_scan(Ctx& c, const VarIO& v, const int* seg_list, int njobs, dou
         PCB_CUDA(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), c.stream));
     }
     const unsigned grid = 2u * static_cast<unsigned>(njobs) * static_cast<unsigned>(R.cl);
-    k_var_scan<<<grid, ST, smem, c.stream>>>(v.st, seg_list, K, R.posl, R.ocnt, xr, tot, R.cl, R.rcap, prof);
+    uint32_t pf = 0;  // L2 prefetch distance in CTAs: one wave of resident CTAs
+    if (const char* e = std::getenv("PCB_SCAN_PF")) {
+        pf = static_cast<uint32_t>(std::atoi(e));
+    } else {
+        int per_sm = 0, nsm = 0;
+        PCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_var_scan, ST, smem));
+        PCB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
+        pf = static_cast<uint32_t>(per_sm * nsm);
+    }
+    k_var_scan<<<grid, ST, smem, c.stream>>>(v.st, seg_list, K, R.posl, R.ocnt, xr, tot, R.cl, R.rcap, prof, pf);
     c.count_launch();
     if (prof) {
         unsigned long long h[8];
