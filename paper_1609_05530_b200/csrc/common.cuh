@@ -21,7 +21,7 @@ struct BlockState {
     double theta;  // current iterate (theta-hat once converged)
     double lo, hi; // root bracket
     double step;   // last accepted step
-    double S, H;   // last score / Hessian sums
+    double th_prev, h_prev;  // theta and Hessian sum of the previous Newton pass (curvature of the score)
     double loglik, sigma2;
     double info_sum;   // sum hess at theta-hat
     double c1, c2;     // sum u*cross1, sum v*cross2 at theta-hat

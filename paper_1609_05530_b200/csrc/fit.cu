@@ -65,8 +65,20 @@ __device__ double invert_table(const double* rho, const double* th, double r) {
 // Safeguarded Newton step on the pseudo-score (mirrors oracle/mpl_driver.hpp
 // Driver::fit's bracket / boundary rules; SPEC.md:242 keeps iterates inside
 // the domain). Runs in one thread per block.
-__device__ void newton_update(BlockState& s, int fam, double S, double H, double tol, unsigned* running) {
+// f64: the sums come from fp64 per-point arithmetic. Then a step inside the
+// tolerance ends the fit only if the quadratic-convergence residual it
+// leaves, |S''| d^2 / (2|H|) with S'' = dH/dtheta from the previous pass,
+// is below 1e-13 max(1, |theta|); otherwise the step is taken and one more
+// pass runs (score curvature is large near the Gumbel boundary theta = 1,
+// where sigma2 also amplifies any error of theta-hat).
+__device__ void newton_update(BlockState& s, int fam, double S, double H, double tol, unsigned* running,
+                              bool f64 = false) {
     s.iters += 1;
+    const double th_prev = s.th_prev, h_prev = s.h_prev;
+    if (isfinite(H)) {
+        s.th_prev = s.theta;
+        s.h_prev = H;
+    }
     if (tol < 0.0) {  // warm-up pass (fp32 per-point arithmetic): move theta, decide nothing
         if (isfinite(S) && isfinite(H) && H < 0.0) {
             double cand = s.theta - S / H;
@@ -75,8 +87,6 @@ __device__ void newton_update(BlockState& s, int fam, double S, double H, double
         }
         return;
     }
-    s.S = S;
-    s.H = H;
     double t = s.theta;
     if (!isfinite(S) || !isfinite(H)) {
         s.status = kNotConverged;
@@ -97,7 +107,12 @@ __device__ void newton_update(BlockState& s, int fam, double S, double H, double
     double cand = NAN;
     if (H < 0.0) {
         cand = t - S / H;
-        if (fabs(cand - t) <= tol * fmax(1.0, fabs(t))) {
+        bool small = fabs(cand - t) <= tol * fmax(1.0, fabs(t));
+        if (small && f64 && isfinite(h_prev) && th_prev != t) {
+            const double d = cand - t, s2 = (H - h_prev) / (t - th_prev);
+            small = !(fabs(s2) * d * d > 2e-13 * fabs(H) * fmax(1.0, fabs(t)));
+        }
+        if (small) {
             if (!(fam == kGumbel && cand < 1.0)) t = cand;
             s.step = cand - s.theta;
             s.theta = t;
@@ -155,6 +170,8 @@ __global__ void k_init_state(BlockState* st, const Seg* segs, int nseg, const in
     s.theta = theta_in ? theta_in[m] : NAN;
     s.lo = -INFINITY;
     s.hi = INFINITY;
+    s.th_prev = NAN;
+    s.h_prev = NAN;
     s.loglik = NAN;
     s.sigma2 = NAN;
     if (bad && bad[m]) s.status = kBadData;
@@ -346,10 +363,13 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
 // F32: fp32 per-point arithmetic (the warm-up passes, or the fp32 precision
 // mode); TI: the stored pair — float2 (T32 / fp32 T) or double2 (fp64 T,
 // converted at load: Frank to the edge encoding, Gumbel by rounding).
+// Four CTAs per SM: 64 registers (the allocation measured fastest; left to
+// itself the fp64 Gumbel pass takes 80 and loses 1.3 ms per family at C5).
 template <int FAM, class TI, bool F32 = (sizeof(TI) == 8)>
-__global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int nseg, const TI* __restrict__ T,
-                                           double* partials, unsigned* tickets, unsigned* running, double tol) {
-    const uint32_t tile = blockIdx.x;
+__global__ void __launch_bounds__(FT, 4) k_lik(BlockState* st, const Seg* segs, int nseg, const TI* __restrict__ T,
+                                           double* partials, unsigned* tickets, unsigned* running, double tol,
+                                           const uint32_t* tile_list) {
+    const uint32_t tile = tile_list ? tile_list[blockIdx.x] : blockIdx.x;
     const int m = seg_of_tile(segs, nseg, tile);
     const Seg S = segs[m];
     if (st[m].status != kRunning) return;
@@ -468,7 +488,7 @@ __global__ void __launch_bounds__(FT) k_lik(BlockState* st, const Seg* segs, int
     if (!tile_reduce<2>(v, sh, partials, tickets, S, m, tile)) return;
     if (threadIdx.x == 0) {
         BlockState s = st[m];
-        newton_update(s, FAM, v[0], v[1], tol, running);
+        newton_update(s, FAM, v[0], v[1], tol, running, !F32);
         st[m] = s;
     }
 }
@@ -615,17 +635,30 @@ void launch_prepare(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int
 
 template <int FAM>
 void launch_lik(Ctx& c, uint32_t tiles, BlockState* st, const Seg* segs, int K, bool f32, const void* T,
-                double* part, unsigned* tick, unsigned* running, double tol, bool t64 = false) {
+                double* part, unsigned* tick, unsigned* running, double tol, bool t64 = false,
+                const uint32_t* tile_list = nullptr) {
     if (f32 && t64)  // fp32 warm-up arithmetic straight from the fp64 T
         k_lik<FAM, double2, true><<<tiles, FT, 0, c.stream>>>(st, segs, K, static_cast<const double2*>(T), part,
-                                                              tick, running, tol);
+                                                              tick, running, tol, tile_list);
     else if (f32)
         k_lik<FAM, float2><<<tiles, FT, 0, c.stream>>>(st, segs, K, static_cast<const float2*>(T), part, tick,
-                                                       running, tol);
+                                                       running, tol, tile_list);
     else
         k_lik<FAM, double2><<<tiles, FT, 0, c.stream>>>(st, segs, K, static_cast<const double2*>(T), part, tick,
-                                                        running, tol);
+                                                        running, tol, tile_list);
     c.count_launch();
+}
+
+// Tiles of the blocks still running (any order: tile_reduce sums a block's
+// partials in tile order), so a pass that only a few blocks need does not
+// launch, and early-exit, every tile of the family.
+__global__ void k_running_tiles(const BlockState* st, const Seg* segs, int nseg, uint32_t* list, unsigned* count) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= nseg || st[m].status != kRunning) return;
+    const Seg S = segs[m];
+    const uint32_t nt = (S.n + FTILE - 1) / FTILE;
+    const uint32_t at = atomicAdd(count, nt);
+    for (uint32_t q = 0; q < nt; ++q) list[at + q] = S.tile0 + q;
 }
 
 __global__ void k_set_start(BlockState* st, int nseg, const double* theta0) {
@@ -697,7 +730,7 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
     auto* part = c.ws.get_t<double>("fit.partials", static_cast<size_t>(tiles) * 4 + 4);
     auto* tick = c.ws.get_t<unsigned>("fit.tickets", K);
     auto* running = c.ws.get_t<unsigned>("fit.running", 1);
-    auto* h_running = static_cast<unsigned*>(c.host_staging(sizeof(unsigned)));
+    auto* h_running = static_cast<unsigned*>(c.host_staging(2 * sizeof(unsigned)));  // [1]: tile count
     PCB_CUDA(cudaMemcpyAsync(d_segs, segs.data(), K * sizeof(Seg), cudaMemcpyHostToDevice, s));
     PCB_CUDA(cudaMemsetAsync(tick, 0, K * sizeof(unsigned), s));
     PCB_CUDA(cudaMemsetAsync(running, 0, sizeof(unsigned), s));
@@ -775,9 +808,24 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
             const void* Tp = (wp && !warm_t64) ? static_cast<const void*>(T32) : T;
             const double tol = wp ? -1.0 : (fp32T ? kTol32 : kTol64);
             const bool t64 = wp && warm_t64;
+            uint32_t grid = tiles;
+            const uint32_t* tl = nullptr;
+            if (pass > 0 && *h_running * 8u <= static_cast<unsigned>(K)) {  // few blocks left: their tiles only
+                auto* list = c.ws.get_t<uint32_t>("fit.tile_list", tiles);
+                auto* cnt = c.ws.get_t<unsigned>("fit.tile_count", 1);
+                PCB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned), s));
+                k_running_tiles<<<(K + 127) / 128, 128, 0, s>>>(st, d_segs, K, list, cnt);
+                c.count_launch();
+                unsigned* h_cnt = h_running + 1;
+                PCB_CUDA(cudaMemcpyAsync(h_cnt, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+                PCB_CUDA(cudaStreamSynchronize(s));
+                grid = *h_cnt;
+                tl = list;
+                if (grid == 0) break;
+            }
             PCB_CUDA(cudaEventRecord(ev[6], s));
-            if (fam == kFrank) launch_lik<kFrank>(c, tiles, st, d_segs, K, f32, Tp, part, tick, running, tol, t64);
-            else launch_lik<kGumbel>(c, tiles, st, d_segs, K, f32, Tp, part, tick, running, tol, t64);
+            if (fam == kFrank) launch_lik<kFrank>(c, grid, st, d_segs, K, f32, Tp, part, tick, running, tol, t64, tl);
+            else launch_lik<kGumbel>(c, grid, st, d_segs, K, f32, Tp, part, tick, running, tol, t64, tl);
             PCB_CUDA(cudaEventRecord(ev[7], s));
             PCB_CUDA(cudaMemcpyAsync(h_running, running, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
             PCB_CUDA(cudaStreamSynchronize(s));

@@ -469,3 +469,41 @@ def test_fit_extreme_parameters(ctx, orc, fam, theta):
     got = pcb.fit_blocks(fam, X, off, ctx=ctx)
     want = orc.fit_blocks(fam, X.col1, X.col2, off)
     check_records(got, want, TOL64)
+
+
+def test_frank_near_zero_conditioning(ctx, orc):
+    """Frank estimate ~1e-3 on 240 rows (a fuzz case): both the device and the
+    oracle against a 60-digit evaluation (tests/golden/make_frank_near_zero.py),
+    and device vs oracle within the conditioning-scaled bar of
+    tests/test_oracle.py::frank_cond_tol (1e-9 x (0.03/|theta|)^2 below |theta| = 0.03)."""
+    import json
+    import os
+
+    from test_oracle import frank_cond_tol
+
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    inp = json.load(open(os.path.join(gold, "frank_near_zero_input.json")))
+    hp = json.load(open(os.path.join(gold, "frank_near_zero_expected.json")))
+    c1, c2 = np.asarray(inp["c1"]), np.asarray(inp["c2"])
+    off = np.array([0, len(c1)], np.uint64)
+    (g,) = pcb.fit_blocks(1, pcb.DataMatrix(c1, c2), off, ctx=ctx)
+    (w,) = orc.fit_blocks(1, c1, c2, off)
+    assert g.converged and w.converged
+    assert rel(g.theta_hat, hp["theta_hat"]) <= 5e-9, (g.theta_hat, hp["theta_hat"])
+    assert rel(g.sigma2, hp["sigma2"]) <= 5e-8, (g.sigma2, hp["sigma2"])
+    tol = frank_cond_tol(w.theta_hat)
+    assert rel(g.theta_hat, w.theta_hat) <= tol and rel(g.sigma2, w.sigma2) <= tol
+
+
+@pytest.mark.parametrize("theta,seed", [(1.003, 11), (1.006, 12), (1.01, 13), (1.006, 14)])
+def test_gumbel_near_boundary(ctx, orc, theta, seed):
+    """Gumbel estimates just above the independence boundary theta = 1: the
+    score is strongly curved there and sigma2 amplifies any error of
+    theta-hat ~100x, so the fp64 stop must account for the residual the last
+    Newton step leaves (fit.cu newton_update); found by tools/fuzz_fit.py."""
+    n = 120000
+    X = pcb.sample_matrix(2, theta, n, 1, base_seed=0x160905530 + seed, ctx=ctx)
+    off = np.array([0, n], np.uint64)
+    (g,) = pcb.fit_blocks(2, X, off, ctx=ctx)
+    (w,) = orc.fit_blocks(2, np.asarray(X.col1), np.asarray(X.col2), off)
+    check_records([g], [w], TOL64)

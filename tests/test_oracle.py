@@ -189,3 +189,26 @@ def test_counter_stream_is_splitmix(orc):
         z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
         z ^= z >> 31
         assert orc.lib.orc_unit_draw(seed, d) == ((z >> 11) + 0.5) * 2.0**-53
+
+
+def frank_cond_tol(theta_hat, base=1e-9, theta_c=0.03):
+    """Parity tolerance for Frank estimates near 0: the reference's formulas
+    (copula.hpp:147-172) cancel terms of size 1/t and 1/t^2, so any fp64
+    evaluation carries ~eps/t^2 relative error below |t| ~ theta_c
+    (tests/golden/make_frank_near_zero.py measures it against 60 digits)."""
+    return base * max(1.0, (theta_c / max(abs(theta_hat), 1e-300)) ** 2)
+
+
+def test_frank_near_zero_against_high_precision(orc):
+    """A 240-row Frank block with estimate ~1e-3: the oracle (and, in
+    test_gpu_parity, the device) against a 60-digit evaluation of the same
+    estimator. Both fp64 evaluations sit ~1e-9 (theta) / ~1e-8 (sigma2) from
+    the truth here, which bounds how closely they can agree."""
+    inp = json.load(open(os.path.join(GOLD, "frank_near_zero_input.json")))
+    hp = json.load(open(os.path.join(GOLD, "frank_near_zero_expected.json")))
+    c1, c2 = np.asarray(inp["c1"]), np.asarray(inp["c2"])
+    (rec,) = orc.fit_blocks(1, c1, c2, np.array([0, len(c1)], np.uint64))
+    assert rec.converged
+    assert rel(rec.theta_hat, hp["theta_hat"]) <= 3e-9, (rec.theta_hat, hp["theta_hat"])
+    assert rel(rec.sigma2, hp["sigma2"]) <= 2e-8, (rec.sigma2, hp["sigma2"])
+    assert rel(rec.theta_hat, hp["theta_hat"]) <= frank_cond_tol(hp["theta_hat"])

@@ -16,6 +16,8 @@ from scipy.special import ndtri
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1609_05530_b200 as pcb  # noqa: E402
 from oracle.oracle import oracle_lib  # noqa: E402
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+from test_oracle import frank_cond_tol  # noqa: E402
 
 TRANSFORMS = [lambda u: u, lambda u: ndtri(u), lambda u: np.tan(np.pi * (u - 0.5)), lambda u: -np.log1p(-u),
               lambda u: np.exp(4.0 * ndtri(u))]
@@ -47,9 +49,12 @@ def run(secs, seed, ctx=None, orc=None):
         for m, (a, b) in enumerate(zip(got, want)):
             ok = bool(a.converged) == bool(b.converged)
             if ok and b.converged:
+                # Frank near theta = 0: the reference formulas lose ~eps/theta^2
+                # (tests/test_oracle.py::frank_cond_tol, tests/golden/make_frank_near_zero.py)
+                tol = frank_cond_tol(b.theta_hat) if fam == 1 else 1e-9
                 e = max(rel(a.theta_hat, b.theta_hat), rel(a.sigma2, b.sigma2))
-                worst = max(worst, e)
-                ok = e <= 1e-9
+                worst = max(worst, e * 1e-9 / tol)
+                ok = e <= tol
             if not ok:
                 os.makedirs("gpurun_out", exist_ok=True)
                 np.savez("gpurun_out/fuzz_fit_fail.npz", c1=c1, c2=c2, off=off, fam=fam, theta=theta)
@@ -57,7 +62,7 @@ def run(secs, seed, ctx=None, orc=None):
                       f"{(a.theta_hat, a.sigma2, a.converged)} vs {(b.theta_hat, b.sigma2, b.converged)}", flush=True)
                 raise AssertionError("fuzz mismatch (inputs saved under gpurun_out/)")
         cases += 1
-    return f"fuzz fit ok: {cases} cases in {time.time() - t0:.0f} s; worst rel error {worst:.2e}"
+    return f"fuzz fit ok: {cases} cases in {time.time() - t0:.0f} s; worst rel error {worst:.2e} (in units of the bar x 1e-9)"
 
 
 if __name__ == "__main__":
