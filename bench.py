@@ -154,6 +154,67 @@ def cpu_reference(args, steps, warmup, subsets_per_step):
     return pts, dt, kind, cores
 
 
+def cpu_leg_and_parity(args, cols, gathered, first, last, q, rows, world):
+    """cpu_baseline on a bounded sample + parity of the GPU records on it.
+    Subsets are spread over this rank's whole range (first, middle, last ...),
+    their input columns copied from the device (identical bytes)."""
+    from oracle.oracle import oracle_lib, ref_lib
+    lib = ref_lib()
+    kind = "reference" if lib is not None else "port"
+    lib = lib or oracle_lib()
+    cores = os.cpu_count() or 1
+    kl = last - first
+    sub = max(1, min(kl, args.cpu_subsets // 3))
+    picks = np.unique(np.linspace(0, kl - 1, sub).round().astype(np.int64))
+    tot_pts, tot_s = 0, 0.0
+    worst_t, worst_s, worst_c, mism = 0.0, 0.0, 0.0, 0
+    per_family = {}
+    for name, fam, th in FAMILIES:
+        c1d, c2d = cols[name]
+        b0 = picks * q
+        n_last = rows - (kl - 1) * q
+        lens = np.where(picks == kl - 1, n_last, q)
+        h1 = np.concatenate([c1d[int(a):int(a + ln)].cpu().numpy() for a, ln in zip(b0, lens)])
+        h2 = np.concatenate([c2d[int(a):int(a + ln)].cpu().numpy() for a, ln in zip(b0, lens)])
+        off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+        t0 = time.perf_counter()
+        recs = lib.fit_blocks(fam, h1, h2, off, workers=cores)
+        tc_cpu, _, _ = lib.combine(recs)
+        tot_s += time.perf_counter() - t0
+        tot_pts += int(off[-1])
+        arr = gathered[name].cpu().numpy().view(np.uint8).reshape(-1, 48)
+        g = arr[picks + (first if world > 1 else 0)]
+        gth = g[:, 0:8].copy().view(np.float64).ravel()
+        gs2 = g[:, 8:16].copy().view(np.float64).ravel()
+        gconv = g[:, 36:40].copy().view(np.int32).ravel()
+        cth = np.array([r.theta_hat for r in recs])
+        cs2 = np.array([r.sigma2 for r in recs])
+        cconv = np.array([int(bool(r.converged)) for r in recs])
+        mism += int(np.sum(cconv != (gconv != 0)))
+        ok = cconv.astype(bool)
+        rt = float(np.max(np.abs(gth[ok] - cth[ok]) / np.abs(cth[ok]))) if ok.any() else 0.0
+        rs = float(np.max(np.abs(gs2[ok] - cs2[ok]) / np.abs(cs2[ok]))) if ok.any() else 0.0
+        # combine of the same subsets' GPU records (fixed block order)
+        w = np.where(gconv != 0, 1.0 / gs2, 0.0)
+        tc_gpu = float(np.sum(w * np.where(gconv != 0, gth, 0.0)) / np.sum(w))
+        rc = abs(tc_gpu - tc_cpu) / abs(tc_cpu)
+        worst_t, worst_s, worst_c = max(worst_t, rt), max(worst_s, rs), max(worst_c, rc)
+        per_family[name] = {"blocks": int(len(picks)), "max_rel_theta": rt, "max_rel_sigma2": rs,
+                            "rel_theta_combined_of_sample": rc}
+    tol = 1e-9
+    parity = {"blocks_per_family": int(len(picks)), "spread": "evenly over the subset range (first..last)",
+              "inputs": "device bytes copied to host", "checker": kind, "max_rel_theta": worst_t,
+              "max_rel_sigma2": worst_s, "max_rel_theta_combined_of_sample": worst_c,
+              "converged_mismatch": mism, "tol": tol,
+              "ok": bool(worst_t <= tol and worst_s <= tol and worst_c <= tol and mism == 0),
+              "per_family": per_family}
+    cpu = {"value": tot_pts / tot_s, "unit": "points/s", "cores": cores, "kind": kind,
+           "sample": f"{len(picks)} subsets x {q} points per family (3 families) spread over the C5 partition, "
+                     f"inputs = the GPU arm's device bytes; fit by Newton on the score root (SPEC-literal Brent "
+                     f"would be 4-7x slower, SURVEY.md §0)"}
+    return cpu, parity
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -364,6 +425,18 @@ def run_ours(args):
         roof["pipeline"] = {"floor_ms_per_step": floor_ms, "frac": floor_ms / ms,
                             "pts_per_s_per_gpu": PIPE_ROOF_PTS,
                             "source": "SURVEY.md §8(d): Gaussian HBM 96 B/pt; Frank/Gumbel FP64 F_pipe (P=4/4.2)"}
+    # ------------------------------------------------------------ cpu_baseline + parity
+    # The reference CPU path (oracle/_ref) fits a spread of this rank's
+    # subsets from the SAME device bytes (D2H of their input columns); the
+    # GPU records of those subsets must match within 1e-9 (SPEC.md:284-301,
+    # north_star), and so must the inverse-variance combine over them.
+    cpu, parity = None, None
+    if rank == 0 and not args.no_cpu:
+        try:
+            cpu, parity = cpu_leg_and_parity(args, cols, gathered, first, last, q, rows, world)
+        except Exception as ex:  # never fail the GPU line on the baseline leg
+            cpu = {"value": None, "unit": "points/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
+
     # ------------------------------------------------------------ e2e
     e2e = None
     if not args.no_e2e:
@@ -407,16 +480,6 @@ def run_ours(args):
                "d2h_bytes_per_step": int(48 * K * len(FAMILIES)), "ms_per_step": dt * 1e3,
                "timing": "host wall clock around the synchronous C-ABI calls (max over ranks)"}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        try:
-            sub = max(1, args.cpu_subsets // 3)
-            pts, dt, kind, cores = cpu_reference(args, 1, 0, sub)
-            cpu = {"value": pts / dt, "unit": "points/s", "cores": cores, "kind": kind,
-                   "sample": f"{sub} subsets x {q} points per family (3 families), C5 partition, same seeds"}
-        except Exception as ex:  # never fail the GPU line on the baseline leg
-            cpu = {"value": None, "unit": "points/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
-
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
@@ -426,7 +489,7 @@ def run_ours(args):
                                    "n=1e9 fp64 pairs per family, K=8000 subsets of 125000, rank->fit->variance->gather->combine",
                        "n_per_family": n, "subsets": K, "subset_rows": q, "parallelism": f"dp{world} (subset shards)",
                        "l2": "inputs (16 GB per family) exceed the 126 MB L2; no flush needed"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roof, "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "kernels": kernels, "results": res,
         }
         print(json.dumps(line), flush=True)

@@ -46,7 +46,14 @@ typedef struct pcb_context pcb_context;
 enum pcb_family { PCB_GAUSSIAN = 0, PCB_FRANK = 1, PCB_GUMBEL = 2 };
 
 /* likelihood-pass arithmetic: fp64, or fp32 per-point terms with fp64
- * accumulation / Newton / variance (BASELINE.json configs[3]) */
+ * accumulation / Newton / variance (BASELINE.json configs[3]). PCB_FP32
+ * applies to the Frank and Gumbel Newton passes; Frank blocks whose iterate
+ * has |theta| < 2 run their decision passes in fp64 arithmetic (the score
+ * cancels terms of size 2/theta, copula.hpp:156-172), and so do Gumbel blocks
+ * with theta < 1.1 (sigma2 amplifies root errors ~100x near theta = 1). The
+ * Gaussian fit has no
+ * per-point likelihood pass (closed-form sufficient statistics from the rank
+ * tables), so PCB_FP32 computes it in fp64. */
 enum pcb_precision { PCB_FP64 = 0, PCB_FP32 = 1 };
 
 /* Partition scheme { Contiguous, Strided } */

@@ -225,18 +225,21 @@ void pipeline_blocks_host(pcb::Ctx& c, int fam, int prec, const double* h1, cons
     auto enqueue = [&](size_t g) {
         const uint64_t r0 = off[groups[g].first], rows = off[groups[g].second] - r0;
         double** d = buf[g & 1];
+        // the buffer's previous user (group g-2) must have finished computing
+        if (g >= 2) PCB_CUDA(cudaStreamWaitEvent(c.copy_stream, c.cev[2 + (g & 1)], 0));
         PCB_CUDA(cudaMemcpyAsync(d[0], h1 + r0, rows * sizeof(double), cudaMemcpyHostToDevice, c.copy_stream));
         PCB_CUDA(cudaMemcpyAsync(d[1], h2 + r0, rows * sizeof(double), cudaMemcpyHostToDevice, c.copy_stream));
         PCB_CUDA(cudaEventRecord(c.cev[g & 1], c.copy_stream));
     };
     enqueue(0);
     for (size_t g = 0; g < groups.size(); ++g) {
-        if (g + 1 < groups.size()) enqueue(g + 1);  // its buffer's previous user (group g-1) has finished
+        if (g + 1 < groups.size()) enqueue(g + 1);  // stream-ordered after group g-1's compute
         PCB_CUDA(cudaStreamWaitEvent(c.stream, c.cev[g & 1], 0));
         const uint64_t b0 = groups[g].first, b1 = groups[g].second, r0 = off[b0];
         std::vector<uint64_t> og(b1 - b0 + 1);
         for (uint64_t b = b0; b <= b1; ++b) og[b - b0] = off[b] - r0;
         pipeline_blocks(c, fam, prec, buf[g & 1][0], buf[g & 1][1], off[b1] - r0, og, d_out + b0);
+        PCB_CUDA(cudaEventRecord(c.cev[2 + (g & 1)], c.stream));
     }
 }
 

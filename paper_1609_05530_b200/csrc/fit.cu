@@ -39,6 +39,22 @@ constexpr int kMaxPasses = 64;
 constexpr double kTol64 = 1e-6;
 constexpr double kTol32 = 1e-6;
 constexpr int kWarmPasses = 2;
+// fp32 likelihood mode: Frank blocks whose iterate has |theta| below this run
+// the pass in fp64 per-point arithmetic (on the same fp32 edge-encoded
+// inputs). The Frank score (copula.hpp:156-172) cancels terms of size ~2/theta,
+// so fp32 per-point sums lose ~eps32 * 2/theta^2 relative there
+// (tools/fp32_edges.py: 1e-4 at theta = 0.3, 0.86 at theta = 0.05).
+#ifndef PCB_FRANK32_EXACT
+#define PCB_FRANK32_EXACT 2.0
+#endif
+constexpr double kFrank32Exact = PCB_FRANK32_EXACT;
+// Likewise Gumbel blocks with theta < 1.1: near the boundary theta = 1 the
+// variance amplifies any error of theta-hat ~100x (a 1e-7 fp32 root error
+// became 1.1e-5 in sigma2 at theta-hat = 1.002).
+#ifndef PCB_GUMBEL32_EXACT
+#define PCB_GUMBEL32_EXACT 1.1
+#endif
+constexpr double kGumbel32Exact = PCB_GUMBEL32_EXACT;
 #ifndef PCB_LIK_UNROLL
 #define PCB_LIK_UNROLL 4
 #endif
@@ -75,6 +91,13 @@ __device__ void newton_update(BlockState& s, int fam, double S, double H, double
                               bool f64 = false) {
     s.iters += 1;
     const double th_prev = s.th_prev, h_prev = s.h_prev;
+    // The curvature estimate below differences this pass's Hessian sum with
+    // the previous pass's, which on the first fp64 pass is an fp32 warm-up
+    // sum. Its rounding can only move the estimated residual by
+    // ~eps32 |H| d^2 / dtheta, i.e. turn a borderline stop into one more fp64
+    // pass (C5: 139 of 8000 Frank and 4 Gumbel blocks, +0.1 / +0.3 ms) -- it
+    // never replaces a curvature estimate by none, which recording fp64
+    // passes only would do for the first fp64 pass.
     if (isfinite(H)) {
         s.th_prev = s.theta;
         s.h_prev = H;
@@ -149,6 +172,9 @@ __device__ void newton_update(BlockState& s, int fam, double S, double H, double
 // Edge encoding for fp32 Frank inputs: p = u (u <= 1/2) or -(1-u) (u > 1/2),
 // computed in fp64, so both u and 1-u keep full fp32 relative precision.
 __device__ __forceinline__ float frank_edge(double u) { return static_cast<float>(u <= 0.5 ? u : -(1.0 - u)); }
+// fp64 value of an edge-encoded input (fp64 T holds u itself)
+__device__ __forceinline__ double frank_decode(float p) { return p >= 0.0f ? static_cast<double>(p) : 1.0 + p; }
+__device__ __forceinline__ double frank_decode(double u) { return u; }
 __device__ __forceinline__ void frank_unedge(float p, float& val, float& comp) {
     if (p >= 0.0f) {
         val = p;
@@ -378,6 +404,7 @@ __global__ void __launch_bounds__(FT, 4) k_lik(BlockState* st, const Seg* segs, 
     const TI* Tb = T + S.begin + base;
     const uint32_t cnt = min(FTILE, S.n - base);
     double v[2] = {0.0, 0.0};
+    bool f64pass = !F32;
     auto warm_pair = [](const TI& p) -> float2 {
         if constexpr (sizeof(TI) == 8) {
             return p;
@@ -410,6 +437,35 @@ __global__ void __launch_bounds__(FT, 4) k_lik(BlockState* st, const Seg* segs, 
                     const TI p = Tb[i];
                     double s, h;
                     gumbel_sh(p.x, p.y, g, s, h);
+                    v[0] += s;
+                    v[1] += h;
+                }
+            }
+        }
+    } else if (tol >= 0.0 && (FAM == kFrank ? fabs(theta) < kFrank32Exact : theta < kGumbel32Exact)) {
+        // fp32 mode, ill-conditioned theta: fp64 arithmetic on the decoded
+        // fp32 inputs (this pass decides convergence in fp64, like the fp64 mode)
+        f64pass = true;
+        if (FAM == kFrank) {
+            const FrankTheta f(theta);
+            for (int k = 0; k < PPT; ++k) {
+                const uint32_t i = k * FT + threadIdx.x;
+                if (i < cnt) {
+                    const TI p = Tb[i];
+                    double s, h;
+                    frank_sh(frank_decode(p.x), frank_decode(p.y), f, s, h);
+                    v[0] += s;
+                    v[1] += h;
+                }
+            }
+        } else {
+            const GumbelTheta g(theta);
+            for (int k = 0; k < PPT; ++k) {
+                const uint32_t i = k * FT + threadIdx.x;
+                if (i < cnt) {
+                    const TI p = Tb[i];
+                    double s, h;
+                    gumbel_sh(static_cast<double>(p.x), static_cast<double>(p.y), g, s, h);
                     v[0] += s;
                     v[1] += h;
                 }
@@ -488,7 +544,7 @@ __global__ void __launch_bounds__(FT, 4) k_lik(BlockState* st, const Seg* segs, 
     if (!tile_reduce<2>(v, sh, partials, tickets, S, m, tile)) return;
     if (threadIdx.x == 0) {
         BlockState s = st[m];
-        newton_update(s, FAM, v[0], v[1], tol, running, !F32);
+        newton_update(s, FAM, v[0], v[1], tol, running, f64pass);
         st[m] = s;
     }
 }

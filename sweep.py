@@ -76,6 +76,8 @@ def main():
                 for prec, pname in ((0, "fp64"), (1, "fp32")):
                     comb, ms, st = fit(fam, c1, c2, k, prec)
                     rec = {"config": "C4", "family": name, "theta_true": th, "n": n, "K": k, "precision": pname,
+                           # the Gaussian fit has no per-point likelihood pass (sufficient statistics)
+                           "lik_arith": "fp64" if (fam == 0 or prec == 0) else "fp32 (Frank |theta|<2, Gumbel theta<1.1: fp64)",
                            "theta_combined": comb.theta_combined, "blocks_used": int(comb.blocks_used),
                            "theta_full": full.theta_combined,
                            "abs_err_vs_full": abs(comb.theta_combined - full.theta_combined),

@@ -129,6 +129,27 @@ def test_fit_fp32_parity(ctx, orc, fam, theta):
     check_records(got, want, TOL32)
 
 
+# fp32 likelihood path at edge parameters (the cases tools/fp32_edges.py
+# found outside the bar before Frank blocks with |theta| < 2 ran their
+# decision passes in fp64 arithmetic; fit.cu kFrank32Exact): Frank near 0 and
+# around the switch, Gumbel just above the boundary theta = 1. Bar: 1e-5.
+FP32_EDGES = [(1, t) for t in (-0.3, -0.05, 0.05, 0.3, 1.0, 1.9, 2.1, 25.0, -30.0)] + \
+             [(2, t) for t in (1.001, 1.003, 1.006, 1.01, 1.05)] + [(0, 0.0), (0, 0.97), (0, -0.97)]
+
+
+@pytest.mark.parametrize("fam,theta", FP32_EDGES)
+def test_fit_fp32_edge_parameters(ctx, orc, fam, theta):
+    rng = np.random.default_rng(abs(hash((fam, theta))) % 2**32)
+    for _ in range(3):
+        n = int(rng.integers(2000, 200000))
+        k = int(rng.integers(1, 5))
+        X = pcb.sample_matrix(fam, theta, n, k, base_seed=int(rng.integers(1, 2**62)), ctx=ctx)
+        off = orc.partition(n, k)
+        got = pcb.fit_blocks(fam, X, off, precision=pcb.Precision.fp32, ctx=ctx)
+        want = orc.fit_blocks(fam, X.col1, X.col2, off)
+        check_records(got, want, TOL32)
+
+
 @pytest.mark.parametrize("fam,theta", FAMS)
 def test_fit_from_pseudo_sample(ctx, orc, fam, theta):
     n = 5000

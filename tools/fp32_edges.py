@@ -10,7 +10,7 @@ import paper_1609_05530_b200 as pcb
 from oracle.oracle import oracle_lib
 orc=oracle_lib(); ctx=pcb.Context(0)
 g=np.random.default_rng(5); worst=0; bad=0; cases=0
-for fam, thetas in ((2,[1.001,1.003,1.006,1.01,1.05]), (1,[-0.3,-0.05,0.05,0.3,25.0,-30.0]), (0,[0.0,0.97,-0.97])):
+for fam, thetas in ((2,[1.001,1.003,1.006,1.01,1.05]), (1,[-0.3,-0.05,0.05,0.3,1.0,1.5,1.9,2.1,3.0,25.0,-30.0]), (0,[0.0,0.97,-0.97])):
     for th in thetas:
         for rep in range(3):
             n=int(g.integers(2000,200000)); k=int(g.integers(1,5))
