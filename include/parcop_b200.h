@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define PCB_ABI_VERSION 1
+#define PCB_ABI_VERSION 2
 
 typedef struct pcb_context pcb_context;
 
@@ -95,17 +95,31 @@ typedef struct pcb_combined {
     double theta_combined;
     double total_weight;
     uint64_t blocks_used;
+    /* seconds per block, monotonic clock around ranks +
+     * fit + variance (pcb_fit_parallel: the pipeline's wall time / M, since
+     * the blocks run concurrently on the GPUs; 0 from pcb_combine) */
+    double wall_clock_per_block;
 } pcb_combined;
 
 /* ---------------------------------------------------------------- context */
 pcb_context* pcb_create(int device);  /* NULL on failure (no device, ...) */
+/* A context over several devices: the
+ * first device runs every single-device call; pcb_fit_blocks and
+ * pcb_fit_parallel shard their blocks contiguously over all devices (one
+ * host thread per device inside the call, no communication), gather the
+ * 48-byte records to the first device by peer copies (NVLink) and combine
+ * there in block order -- results are bitwise identical for any device list
+ * (SPEC.md:296, 304). A device may be listed more than once (independent
+ * streams on one GPU). */
+pcb_context* pcb_create_multi(const int* devices, int n_devices);
+int pcb_device_count(const pcb_context* ctx);
 void pcb_destroy(pcb_context* ctx);
 const char* pcb_last_error(const pcb_context* ctx);
 int pcb_abi_version(void);
 /* Launch on the caller's cudaStream_t (e.g. torch's current stream); NULL
  * restores the context's own stream. */
 int pcb_set_stream(pcb_context* ctx, void* cuda_stream);
-/* kernels this context launched so far (the bench's gpu_launches evidence) */
+/* kernels this context launched so far, all devices (the bench's gpu_launches evidence) */
 uint64_t pcb_launch_count(const pcb_context* ctx);
 /* per-stage device milliseconds of the last pipeline call:
  * [0] rank [1] prepare+init [2] likelihood passes [3] variance [4] finalize

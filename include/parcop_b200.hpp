@@ -4,21 +4,40 @@
 // types as /root/reference/proj/include/parcop (present pieces) and
 // /root/reference/SPEC.md (absent estimator / partition-combine modules).
 //
-//   normalized_ranks     pseudo_obs.hpp:71-77
 //   pseudo_loglik
 //   fit
 //   asymptotic_variance
-//   partition
+//   partition            SPEC.md:275-283  (Partition holds the blocks)
 //   combine
-//   fit_parallel
+//   fit_parallel         SPEC.md:293-301  (wall_clock_per_block filled)
+//   b200::normalized_ranks  pseudo_obs.hpp:71-77 on the GPU (opt-in name)
 //
-// Include this header INSTEAD of the reference headers (the types below
-// mirror pseudo_obs.hpp:15-28 and copula.hpp:25). Link -lparcop_b200.
+// Types. When the reference headers are on the include path
+// (`-I…/proj/include`), this header includes <parcop/copula.hpp> and uses
+// the reference's own DataMatrix, PseudoSample (pseudo_obs.hpp:15-28) and
+// CopulaFamily (copula.hpp:25), so a translation unit can mix the two freely
+// (sample with parcop::sample_matrix, fit with parcop::fit_parallel). It
+// defines only the SPEC types the reference lacks (FitResult, Scheme,
+// Partition, CombinedResult). The reference's parcop::normalized_ranks stays
+// the CPU one; the device version is parcop::b200::normalized_ranks. Without
+// the reference headers (or with PARCOP_B200_STANDALONE_TYPES defined), the
+// three types are defined here with the reference's layout and
+// parcop::normalized_ranks is the device version.
+// (The reference's normal.hpp:21 needs std::numbers::inv_sqrt2, which C++20
+// lacks: reference callers already compile it with their own definition,
+// e.g. oracle/shim.hpp.)
+//
+// Devices. One context per host thread: device 0 unless
+// parcop::b200::set_device / set_devices is called first on that thread.
+// With several devices, fit_parallel shards the blocks over all of them
+// (pcb_create_multi) and the result is bitwise the same.
+//
 // Errors: std::invalid_argument / std::domain_error exactly where the
 // reference throws them; std::runtime_error for device failures and for a
-// combine with no converged block.
+// combine with no converged block. Link -lparcop_b200.
 #pragma once
 
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <memory>
@@ -28,11 +47,18 @@
 
 #include "parcop_b200.h"
 
+#if !defined(PARCOP_B200_STANDALONE_TYPES) && defined(__has_include)
+#if __has_include(<parcop/copula.hpp>)
+#define PARCOP_B200_REFERENCE_TYPES 1
+#endif
+#endif
+
+#if defined(PARCOP_B200_REFERENCE_TYPES)
+#include <parcop/copula.hpp>  // CopulaFamily (copula.hpp:25); DataMatrix, PseudoSample (pseudo_obs.hpp:15-28)
+#else
 namespace parcop {
-inline namespace b200 {
 
 enum class CopulaFamily { Gaussian, Frank, Gumbel };  // copula.hpp:25
-enum class Scheme { Contiguous, Strided };            // SPEC.md:264
 
 struct DataMatrix {  // pseudo_obs.hpp:15-20
     std::vector<double> col1;
@@ -46,6 +72,29 @@ struct PseudoSample {  // pseudo_obs.hpp:23-28
     std::size_t rows() const { return u1.size(); }
 };
 
+inline void validate_data(const DataMatrix& x) {  // pseudo_obs.hpp:30-37
+    if (x.col1.size() != x.col2.size()) throw std::invalid_argument("data matrix: columns differ in length");
+    if (x.rows() < 2) throw std::invalid_argument("data matrix: need at least 2 rows");
+    for (std::size_t i = 0; i < x.rows(); ++i)
+        if (!std::isfinite(x.col1[i]) || !std::isfinite(x.col2[i]))
+            throw std::domain_error("data matrix: non-finite value");
+}
+
+inline void validate_pseudo_sample(const PseudoSample& u) {  // pseudo_obs.hpp:79-88
+    if (u.u1.size() != u.u2.size()) throw std::invalid_argument("pseudo sample: columns differ in length");
+    for (std::size_t i = 0; i < u.rows(); ++i)
+        if (!(u.u1[i] > 0.0 && u.u1[i] < 1.0) || !(u.u2[i] > 0.0 && u.u2[i] < 1.0))
+            throw std::domain_error("pseudo sample: values must lie strictly in (0,1)");
+}
+
+}  // namespace parcop
+#endif
+
+namespace parcop {
+
+// ---------------------------------------------------- SPEC types the reference lacks
+enum class Scheme { Contiguous, Strided };  // SPEC.md:264
+
 struct FitResult {
     double theta_hat = 0.0;
     double sigma2 = 0.0;
@@ -55,19 +104,24 @@ struct FitResult {
     bool converged = false;
 };
 
-struct Partition {  // SPEC.md:263-267 (row offsets of the scheme's row order)
-    std::vector<std::uint64_t> offsets;
+struct Partition {
+    std::vector<DataMatrix> blocks;  // ordered row-blocks, pairwise disjoint, covering X
     Scheme scheme = Scheme::Contiguous;
-    std::size_t blocks() const { return offsets.empty() ? 0 : offsets.size() - 1; }
+    // B200 extension: the blocks' row offsets in the scheme's row order
+    // (Contiguous: rows of X; Strided: X gathered so block m = rows i ≡ m mod M)
+    std::vector<std::uint64_t> offsets;
+    std::size_t size() const { return blocks.size(); }
 };
 
 struct CombinedResult {
     double theta_combined = 0.0;
     std::vector<FitResult> per_block;
     std::vector<double> weights;
-    double wall_clock_per_block = 0.0;
+    double wall_clock_per_block = 0.0;  // seconds
     std::size_t blocks_used = 0;
 };
+
+namespace b200 {
 
 namespace detail {
 
@@ -79,10 +133,8 @@ inline void rethrow(pcb_context* ctx, int rc) {
     throw std::runtime_error(msg);
 }
 
-// One context per host thread (SURVEY.md §8(b) threading rule), device 0
-// unless set_device() is called first on that thread.
 struct CtxHolder {
-    int device = 0;
+    std::vector<int> devices{0};
     pcb_context* ctx = nullptr;
     ~CtxHolder() {
         if (ctx) pcb_destroy(ctx);
@@ -95,7 +147,7 @@ inline CtxHolder& holder() {
 inline pcb_context* ctx() {
     CtxHolder& h = holder();
     if (!h.ctx) {
-        h.ctx = pcb_create(h.device);
+        h.ctx = pcb_create_multi(h.devices.data(), static_cast<int>(h.devices.size()));
         if (!h.ctx) throw std::runtime_error(pcb_last_error(nullptr));
     }
     return h.ctx;
@@ -118,15 +170,19 @@ inline void check_pseudo(const PseudoSample& u) {
 
 }  // namespace detail
 
-inline void set_device(int device) {
+// The GPUs this thread's context spans (default {0}).
+inline void set_devices(const std::vector<int>& devices) {
+    if (devices.empty()) throw std::invalid_argument("set_devices: need at least one device");
     detail::CtxHolder& h = detail::holder();
     if (h.ctx) {
         pcb_destroy(h.ctx);
         h.ctx = nullptr;
     }
-    h.device = device;
+    h.devices = devices;
 }
+inline void set_device(int device) { set_devices({device}); }
 
+// pseudo_obs.hpp:71-77 on the device, bit-identical to the reference.
 inline PseudoSample normalized_ranks(const DataMatrix& x) {
     if (x.col1.size() != x.col2.size()) throw std::invalid_argument("data matrix: columns differ in length");
     if (x.rows() < 2) throw std::invalid_argument("data matrix: need at least 2 rows");
@@ -169,13 +225,27 @@ inline double asymptotic_variance(CopulaFamily f, double theta_hat, const Pseudo
     return s2;
 }
 
+// the blocks themselves (row copies), scheme order.
 inline Partition partition(const DataMatrix& x, std::size_t m, Scheme scheme = Scheme::Contiguous) {
     if (m < 1) throw std::invalid_argument("partition: need M >= 1");
+    if (x.col1.size() != x.col2.size()) throw std::invalid_argument("data matrix: columns differ in length");
     Partition p;
     p.scheme = scheme;
     p.offsets.resize(m + 1);
     if (pcb_partition(x.rows(), m, static_cast<int>(scheme), p.offsets.data()) != PCB_OK)
         throw std::invalid_argument("partition: block below the 30-row floor");
+    p.blocks.resize(m);
+    for (std::size_t b = 0; b < m; ++b) {
+        DataMatrix& blk = p.blocks[b];
+        const std::size_t len = static_cast<std::size_t>(p.offsets[b + 1] - p.offsets[b]);
+        blk.col1.resize(len);
+        blk.col2.resize(len);
+        for (std::size_t k = 0; k < len; ++k) {
+            const std::size_t row = scheme == Scheme::Contiguous ? static_cast<std::size_t>(p.offsets[b]) + k : b + k * m;
+            blk.col1[k] = x.col1[row];
+            blk.col2[k] = x.col2[row];
+        }
+    }
     return p;
 }
 
@@ -197,8 +267,9 @@ inline CombinedResult combine(const std::vector<FitResult>& results) {
     return out;
 }
 
-// `workers` is kept for source compatibility; blocks run on the GPU's SMs
-// and the result is bitwise independent of it.
+// `workers` is kept for source compatibility; blocks run on the GPUs' SMs
+// and the result is bitwise independent of it. Host columns
+// (pinned or pageable) stream to the device(s) while earlier blocks compute.
 inline CombinedResult fit_parallel(CopulaFamily f, const DataMatrix& x, std::size_t m, std::size_t workers = 0,
                                    Scheme scheme = Scheme::Contiguous) {
     (void)workers;
@@ -212,9 +283,23 @@ inline CombinedResult fit_parallel(CopulaFamily f, const DataMatrix& x, std::siz
                                         static_cast<int>(scheme), per.data(), out.weights.data(), &cr));
     out.theta_combined = cr.theta_combined;
     out.blocks_used = static_cast<std::size_t>(cr.blocks_used);
+    out.wall_clock_per_block = cr.wall_clock_per_block;
     out.per_block.reserve(m);
     for (const auto& r : per) out.per_block.push_back(detail::to_fit(r));
     return out;
+}
+
+// Device sampler (copula.hpp:359-410 transforms over counter-based
+// splitmix64 streams): n rows as `blocks` seeded blocks.
+inline DataMatrix sample_matrix_device(CopulaFamily f, double theta, std::size_t n, std::size_t blocks = 1,
+                                       std::uint64_t base_seed = 0x160905530ull) {
+    DataMatrix x;
+    x.col1.resize(n);
+    x.col2.resize(n);
+    pcb_context* c = detail::ctx();
+    detail::rethrow(c, pcb_sample(c, static_cast<int>(f), theta, n, blocks, 0, blocks, base_seed, x.col1.data(),
+                                  x.col2.data()));
+    return x;
 }
 
 // sim_study rel_l1 / rel_l2, tensor Gauss-Legendre on device
@@ -233,4 +318,20 @@ inline double rel_l2(CopulaFamily f, double theta_a, double theta_b, int quad_no
 }
 
 }  // namespace b200
+
+// The SPEC operations the reference does not implement, under their SPEC
+// names (no reference declaration to collide with).
+using b200::asymptotic_variance;
+using b200::combine;
+using b200::fit;
+using b200::fit_parallel;
+using b200::partition;
+using b200::pseudo_loglik;
+using b200::rel_l1;
+using b200::rel_l2;
+using b200::set_device;
+#if !defined(PARCOP_B200_REFERENCE_TYPES)
+using b200::normalized_ranks;  // standalone: no reference normalized_ranks exists
+#endif
+
 }  // namespace parcop

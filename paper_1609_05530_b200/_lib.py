@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("PCB_LIB_PATH") or os.path.join(HERE, "libparcop_b200.
 
 # Every symbol include/parcop_b200.h declares (tests check the export table).
 SYMBOLS = (
-    "pcb_create", "pcb_destroy", "pcb_last_error", "pcb_abi_version", "pcb_set_stream", "pcb_launch_count",
+    "pcb_create", "pcb_create_multi", "pcb_device_count", "pcb_destroy", "pcb_last_error", "pcb_abi_version", "pcb_set_stream", "pcb_launch_count",
     "pcb_stage_times", "pcb_rank_paths", "pcb_trim", "pcb_normalized_ranks", "pcb_pseudo_loglik", "pcb_fit",
     "pcb_asymptotic_variance", "pcb_partition", "pcb_combine", "pcb_fit_blocks", "pcb_fit_parallel", "pcb_sample",
     "pcb_measure_fp64_peak", "pcb_rel_error", "pcb_cdf", "pcb_spearman_rho", "pcb_kendall_tau",
@@ -43,7 +43,8 @@ class FitResultC(C.Structure):
 class CombinedC(C.Structure):
     """pcb_combined (SPEC.md:268-272 CombinedResult scalars)."""
 
-    _fields_ = [("theta_combined", C.c_double), ("total_weight", C.c_double), ("blocks_used", C.c_uint64)]
+    _fields_ = [("theta_combined", C.c_double), ("total_weight", C.c_double), ("blocks_used", C.c_uint64),
+                ("wall_clock_per_block", C.c_double)]
 
 
 _lib = None
@@ -63,6 +64,8 @@ def load():
     P = C.POINTER
     sig = {
         "pcb_create": ([i], vp),
+        "pcb_create_multi": ([P(i), i], vp),
+        "pcb_device_count": ([vp], i),
         "pcb_destroy": ([vp], None),
         "pcb_last_error": ([vp], C.c_char_p),
         "pcb_abi_version": ([], i),

@@ -5,15 +5,27 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <chrono>
+#include <condition_variable>
+#include <exception>
+#include <memory>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/parcop_b200.h"
 #include "internal.hpp"
 
+// A context spans one or more devices (pcb_create_multi). `c` is the first
+// device: every single-device entry point runs there. fit_blocks and
+// fit_parallel shard their blocks over all devices.
 struct pcb_context {
     pcb::Ctx c;
+    std::vector<std::unique_ptr<pcb::Ctx>> peers;  // devices 2..G of a multi-device context
+    int ndev() const { return 1 + static_cast<int>(peers.size()); }
+    pcb::Ctx& dev(int g) { return g == 0 ? c : *peers[g - 1]; }
 };
 
 namespace {
@@ -181,6 +193,15 @@ void pipeline_blocks(pcb::Ctx& c, int fam, int prec, const double* d1, const dou
 // copy stream into two device buffers, so the H2D of group g+1 overlaps the
 // rank/fit/variance of group g. Groups are whole blocks, so every block's
 // result is the same as in one call (bitwise).
+//
+// The copies are issued by a stager thread: with pinned columns
+// cudaMemcpyAsync returns at once; with pageable columns (a caller's
+// std::vector) the driver stages each copy through its own pinned buffers and
+// blocks the issuing thread until the bytes are staged -- on the stager
+// thread that wait overlaps the device pipeline of the previous group, which
+// this thread drives (its Newton loop synchronises on the stream per pass).
+// Buffer reuse is stream-ordered: the copy into buffer b waits (on the copy
+// stream) for the compute of the group that last used b.
 void pipeline_blocks_host(pcb::Ctx& c, int fam, int prec, const double* h1, const double* h2, uint64_t n_rows,
                           const std::vector<uint64_t>& off, pcb_fit_result* d_out) {
     const uint64_t K = off.size() - 1;
@@ -222,24 +243,207 @@ void pipeline_blocks_host(pcb::Ctx& c, int fam, int prec, const double* h1, cons
     for (int b = 0; b < 2; ++b)
         for (int j = 0; j < 2; ++j)
             buf[b][j] = c.ws.get_t<double>(std::string("strm.") + char('0' + b) + char('0' + j), maxrows);
-    auto enqueue = [&](size_t g) {
-        const uint64_t r0 = off[groups[g].first], rows = off[groups[g].second] - r0;
-        double** d = buf[g & 1];
-        // the buffer's previous user (group g-2) must have finished computing
-        if (g >= 2) PCB_CUDA(cudaStreamWaitEvent(c.copy_stream, c.cev[2 + (g & 1)], 0));
-        PCB_CUDA(cudaMemcpyAsync(d[0], h1 + r0, rows * sizeof(double), cudaMemcpyHostToDevice, c.copy_stream));
-        PCB_CUDA(cudaMemcpyAsync(d[1], h2 + r0, rows * sizeof(double), cudaMemcpyHostToDevice, c.copy_stream));
-        PCB_CUDA(cudaEventRecord(c.cev[g & 1], c.copy_stream));
+    const size_t G = groups.size();
+    std::mutex mu;
+    std::condition_variable cv;
+    size_t copied = 0;     // groups whose copies are enqueued (copy-done event recorded)
+    size_t computed = 0;   // groups whose compute is enqueued (buffer-free event recorded)
+    bool abort = false;
+    std::string stage_err;
+    const int dev = c.device;
+    std::thread stager([&] {
+        try {
+            PCB_CUDA(cudaSetDevice(dev));
+            for (size_t g = 0; g < G; ++g) {
+                const int b = static_cast<int>(g & 1);
+                if (g >= 2) {  // buffer b's previous user is group g-2
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return computed >= g - 1 || abort; });
+                    if (abort) return;
+                    PCB_CUDA(cudaStreamWaitEvent(c.copy_stream, c.cev[2 + b], 0));
+                }
+                const uint64_t r0 = off[groups[g].first], rows = off[groups[g].second] - r0;
+                PCB_CUDA(cudaMemcpyAsync(buf[b][0], h1 + r0, rows * sizeof(double), cudaMemcpyHostToDevice,
+                                         c.copy_stream));
+                PCB_CUDA(cudaMemcpyAsync(buf[b][1], h2 + r0, rows * sizeof(double), cudaMemcpyHostToDevice,
+                                         c.copy_stream));
+                PCB_CUDA(cudaEventRecord(c.cev[b], c.copy_stream));
+                {
+                    std::lock_guard<std::mutex> lk(mu);
+                    copied = g + 1;
+                }
+                cv.notify_all();
+            }
+        } catch (const std::exception& e) {
+            std::lock_guard<std::mutex> lk(mu);
+            stage_err = e.what();
+            abort = true;
+            cv.notify_all();
+        }
+    });
+    try {
+        for (size_t g = 0; g < G; ++g) {
+            const int b = static_cast<int>(g & 1);
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return copied > g || abort; });
+                if (abort) throw pcb::Error(PCB_E_CUDA, "host input staging failed: " + stage_err);
+            }
+            PCB_CUDA(cudaStreamWaitEvent(c.stream, c.cev[b], 0));
+            const uint64_t b0 = groups[g].first, b1 = groups[g].second, r0 = off[b0];
+            std::vector<uint64_t> og(b1 - b0 + 1);
+            for (uint64_t bb = b0; bb <= b1; ++bb) og[bb - b0] = off[bb] - r0;
+            pipeline_blocks(c, fam, prec, buf[b][0], buf[b][1], off[b1] - r0, og, d_out + b0);
+            PCB_CUDA(cudaEventRecord(c.cev[2 + b], c.stream));
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                computed = g + 1;
+            }
+            cv.notify_all();
+        }
+    } catch (...) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            abort = true;
+        }
+        cv.notify_all();
+        stager.join();
+        cudaStreamSynchronize(c.copy_stream);
+        throw;
+    }
+    stager.join();
+}
+
+int device_of(const void* p) {
+    cudaPointerAttributes a;
+    if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? a.device : -1;
+}
+
+// Opens device `device` into `c` (streams, events, constant tables); throws
+// pcb::Error(PCB_E_CUDA) when it is absent or not an sm_100 part.
+void init_ctx(pcb::Ctx& c, int device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw pcb::Error(PCB_E_CUDA, "no CUDA device available (the library has no CPU fallback)");
+    }
+    if (device < 0 || device >= count) throw pcb::Error(PCB_E_CUDA, "device index out of range");
+    cudaDeviceProp prop;
+    PCB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        throw pcb::Error(PCB_E_CUDA,
+                         std::string("device ") + prop.name + " is not sm_100 (this build targets sm_100a only)");
+    PCB_CUDA(cudaSetDevice(device));
+    c.device = device;
+    PCB_CUDA(cudaStreamCreateWithFlags(&c.own_stream, cudaStreamNonBlocking));
+    c.stream = c.own_stream;
+    for (auto& ev : c.ev) PCB_CUDA(cudaEventCreate(&ev));
+    for (auto& ev : c.cev) PCB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    PCB_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    pcb::init_tables();
+}
+
+void close_ctx(pcb::Ctx& c) {
+    if (!c.own_stream) return;
+    cudaSetDevice(c.device);
+    cudaStreamSynchronize(c.stream);
+    c.ws.release();
+    for (auto& ev : c.ev)
+        if (ev) cudaEventDestroy(ev);
+    for (auto& ev : c.cev)
+        if (ev) cudaEventDestroy(ev);
+    if (c.copy_stream) {
+        cudaStreamSynchronize(c.copy_stream);
+        cudaStreamDestroy(c.copy_stream);
+    }
+    if (c.pinned) cudaFreeHost(c.pinned);
+    cudaStreamDestroy(c.own_stream);
+    c.own_stream = nullptr;
+}
+
+// Contiguous block range of shard g of G (sizes differ by <= 1; the same
+// rule as distributed.shard_blocks)
+std::pair<uint64_t, uint64_t> shard_range(uint64_t K, int G, int g) {
+    const uint64_t q = K / G, r = K % G;
+    const uint64_t first = g * q + std::min<uint64_t>(g, r);
+    return {first, first + q + (static_cast<uint64_t>(g) < r ? 1 : 0)};
+}
+
+// fit_parallel's shard step over every device of the context (SURVEY.md
+// §8(e)): device g takes the contiguous block range shard_range(K, G, g), reads
+// its rows from the host (streamed, pipeline_blocks_host) or from the device
+// that holds the columns (peer copy over NVLink when it is another device),
+// and runs rank -> fit -> variance with no communication. Its records are
+// then gathered by peer copies into d_out (device 0, block order), so the
+// combine that follows is bitwise the same for every device count. One host
+// thread per device drives its pipeline (each pipeline synchronises on its
+// own stream per Newton pass).
+void fit_blocks_sharded(pcb_context* ctx, int fam, int prec, const double* col1, const double* col2,
+                        uint64_t n_rows, const std::vector<uint64_t>& off, pcb_fit_result* d_out) {
+    pcb::Ctx& c0 = ctx->c;
+    const uint64_t K = off.size() - 1;
+    const int G = ctx->ndev();
+    const int src1 = device_of(col1), src2 = device_of(col2);
+    const bool host_in = src1 < 0 && src2 < 0;
+    if (G == 1) {
+        if (host_in) {
+            pipeline_blocks_host(c0, fam, prec, col1, col2, n_rows, off, d_out);
+        } else {
+            const double* d1 = dev_in(c0, col1, n_rows, "c1");
+            const double* d2 = dev_in(c0, col2, n_rows, "c2");
+            pipeline_blocks(c0, fam, prec, d1, d2, n_rows, off, d_out);
+        }
+        return;
+    }
+    if (!host_in && (src1 < 0 || src2 < 0 || src1 != src2))
+        throw pcb::Error(PCB_E_INVALID, "columns must both be host or both on one device");
+    std::vector<std::exception_ptr> errs(G);
+    std::vector<pcb_fit_result*> recs(G, nullptr);
+    auto shard = [&](int g) {
+        try {
+            pcb::Ctx& cg = ctx->dev(g);
+            PCB_CUDA(cudaSetDevice(cg.device));
+            const auto [b0, b1] = shard_range(K, G, g);
+            if (b1 == b0) return;
+            const uint64_t r0 = off[b0], rows = off[b1] - r0;
+            std::vector<uint64_t> og(b1 - b0 + 1);
+            for (uint64_t b = b0; b <= b1; ++b) og[b - b0] = off[b] - r0;
+            pcb_fit_result* rec = g == 0 ? d_out + b0 : cg.ws.get_t<pcb_fit_result>("multi.rec", b1 - b0);
+            recs[g] = rec;
+            if (host_in) {
+                pipeline_blocks_host(cg, fam, prec, col1 + r0, col2 + r0, rows, og, rec);
+            } else if (src1 == cg.device) {
+                pipeline_blocks(cg, fam, prec, col1 + r0, col2 + r0, rows, og, rec);
+            } else {
+                double* d1 = cg.ws.get_t<double>("multi.c1", rows);
+                double* d2 = cg.ws.get_t<double>("multi.c2", rows);
+                PCB_CUDA(cudaMemcpyPeerAsync(d1, cg.device, col1 + r0, src1, rows * sizeof(double), cg.stream));
+                PCB_CUDA(cudaMemcpyPeerAsync(d2, cg.device, col2 + r0, src1, rows * sizeof(double), cg.stream));
+                pipeline_blocks(cg, fam, prec, d1, d2, rows, og, rec);
+            }
+            PCB_CUDA(cudaStreamSynchronize(cg.stream));
+        } catch (...) {
+            errs[g] = std::current_exception();
+        }
     };
-    enqueue(0);
-    for (size_t g = 0; g < groups.size(); ++g) {
-        if (g + 1 < groups.size()) enqueue(g + 1);  // stream-ordered after group g-1's compute
-        PCB_CUDA(cudaStreamWaitEvent(c.stream, c.cev[g & 1], 0));
-        const uint64_t b0 = groups[g].first, b1 = groups[g].second, r0 = off[b0];
-        std::vector<uint64_t> og(b1 - b0 + 1);
-        for (uint64_t b = b0; b <= b1; ++b) og[b - b0] = off[b] - r0;
-        pipeline_blocks(c, fam, prec, buf[g & 1][0], buf[g & 1][1], off[b1] - r0, og, d_out + b0);
-        PCB_CUDA(cudaEventRecord(c.cev[2 + (g & 1)], c.stream));
+    std::vector<std::thread> th;
+    for (int g = 1; g < G; ++g) th.emplace_back(shard, g);
+    shard(0);
+    for (auto& t : th) t.join();
+    PCB_CUDA(cudaSetDevice(c0.device));
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    // K-record gather into device 0, block order (48 B per block)
+    for (int g = 1; g < G; ++g) {
+        const auto [b0, b1] = shard_range(K, G, g);
+        if (b1 == b0) continue;
+        PCB_CUDA(cudaMemcpyPeerAsync(d_out + b0, c0.device, recs[g], ctx->dev(g).device,
+                                     (b1 - b0) * sizeof(pcb_fit_result), c0.stream));
     }
 }
 
@@ -249,56 +453,44 @@ extern "C" {
 
 int pcb_abi_version(void) { return PCB_ABI_VERSION; }
 
-pcb_context* pcb_create(int device) {
+pcb_context* pcb_create(int device) { return pcb_create_multi(&device, 1); }
+
+pcb_context* pcb_create_multi(const int* devices, int n_devices) {
+    pcb_context* ctx = nullptr;
     try {
-        int count = 0;
-        cudaError_t e = cudaGetDeviceCount(&count);
-        if (e != cudaSuccess || count == 0) {
-            cudaGetLastError();
-            g_create_error = "no CUDA device available (the library has no CPU fallback)";
-            return nullptr;
+        if (!devices || n_devices < 1) throw pcb::Error(PCB_E_INVALID, "need at least one device");
+        ctx = new pcb_context();
+        init_ctx(ctx->c, devices[0]);
+        for (int g = 1; g < n_devices; ++g) {
+            ctx->peers.emplace_back(new pcb::Ctx());
+            init_ctx(*ctx->peers.back(), devices[g]);
+            // the record gather (and device-resident inputs) go peer to peer over NVLink
+            const int a = devices[0], b = devices[g];
+            int ab = 0, ba = 0;
+            if (a != b && cudaDeviceCanAccessPeer(&ab, a, b) == cudaSuccess && ab &&
+                cudaDeviceCanAccessPeer(&ba, b, a) == cudaSuccess && ba) {
+                cudaSetDevice(a);
+                cudaDeviceEnablePeerAccess(b, 0);
+                cudaSetDevice(b);
+                cudaDeviceEnablePeerAccess(a, 0);
+                cudaGetLastError();  // cudaErrorPeerAccessAlreadyEnabled is fine
+            }
         }
-        if (device < 0 || device >= count) {
-            g_create_error = "device index out of range";
-            return nullptr;
-        }
-        cudaDeviceProp prop;
-        PCB_CUDA(cudaGetDeviceProperties(&prop, device));
-        if (prop.major != 10) {
-            g_create_error = std::string("device ") + prop.name + " is not sm_100 (this build targets sm_100a only)";
-            return nullptr;
-        }
-        PCB_CUDA(cudaSetDevice(device));
-        auto* ctx = new pcb_context();
-        ctx->c.device = device;
-        PCB_CUDA(cudaStreamCreateWithFlags(&ctx->c.own_stream, cudaStreamNonBlocking));
-        ctx->c.stream = ctx->c.own_stream;
-        for (auto& ev : ctx->c.ev) PCB_CUDA(cudaEventCreate(&ev));
-        for (auto& ev : ctx->c.cev) PCB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        PCB_CUDA(cudaStreamCreateWithFlags(&ctx->c.copy_stream, cudaStreamNonBlocking));
-        pcb::init_tables();
+        cudaSetDevice(devices[0]);
         return ctx;
     } catch (const std::exception& ex) {
         g_create_error = ex.what();
+        if (ctx) pcb_destroy(ctx);
         return nullptr;
     }
 }
 
+int pcb_device_count(const pcb_context* ctx) { return ctx ? ctx->ndev() : 0; }
+
 void pcb_destroy(pcb_context* ctx) {
     if (!ctx) return;
-    cudaSetDevice(ctx->c.device);
-    cudaStreamSynchronize(ctx->c.stream);
-    ctx->c.ws.release();
-    for (auto& ev : ctx->c.ev)
-        if (ev) cudaEventDestroy(ev);
-    for (auto& ev : ctx->c.cev)
-        if (ev) cudaEventDestroy(ev);
-    if (ctx->c.copy_stream) {
-        cudaStreamSynchronize(ctx->c.copy_stream);
-        cudaStreamDestroy(ctx->c.copy_stream);
-    }
-    if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
-    if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
+    for (auto& p : ctx->peers) close_ctx(*p);
+    close_ctx(ctx->c);
     delete ctx;
 }
 
@@ -310,7 +502,12 @@ int pcb_set_stream(pcb_context* ctx, void* s) {
     return PCB_OK;
 }
 
-uint64_t pcb_launch_count(const pcb_context* ctx) { return ctx ? ctx->c.launches : 0; }
+uint64_t pcb_launch_count(const pcb_context* ctx) {
+    if (!ctx) return 0;
+    uint64_t n = ctx->c.launches;
+    for (const auto& p : ctx->peers) n += p->launches;
+    return n;
+}
 
 int pcb_stage_times(const pcb_context* ctx, double* ms, int n) {
     if (!ctx || !ms) return 0;
@@ -327,8 +524,13 @@ int pcb_rank_paths(const pcb_context* ctx, uint64_t* counts) {
 
 int pcb_trim(pcb_context* ctx) {
     return guarded(ctx, [&] {
-        PCB_CUDA(cudaStreamSynchronize(ctx->c.stream));
-        ctx->c.ws.release();
+        for (int g = 0; g < ctx->ndev(); ++g) {
+            pcb::Ctx& cg = ctx->dev(g);
+            PCB_CUDA(cudaSetDevice(cg.device));
+            PCB_CUDA(cudaStreamSynchronize(cg.stream));
+            cg.ws.release();
+        }
+        PCB_CUDA(cudaSetDevice(ctx->c.device));
     });
 }
 
@@ -508,6 +710,7 @@ int pcb_combine(pcb_context* ctx, const pcb_fit_result* results, uint64_t n_bloc
         r.theta_combined = h3[0];
         r.total_weight = h3[1];
         r.blocks_used = static_cast<uint64_t>(h3[2]);
+        r.wall_clock_per_block = 0.0;
         if (is_device_ptr(out)) PCB_CUDA(cudaMemcpy(out, &r, sizeof r, cudaMemcpyHostToDevice));
         else *out = r;
         none = r.blocks_used == 0;
@@ -528,13 +731,7 @@ int pcb_fit_blocks(pcb_context* ctx, int family, int precision, const double* co
         if (!col1 || !col2 || !out) throw pcb::Error(PCB_E_INVALID, "NULL pointer");
         const auto off = check_offsets(seg_offsets, n_seg, n_rows, 2);
         DevOut<pcb_fit_result> o(c, out, n_seg, "fit");
-        if (!is_device_ptr(col1) && !is_device_ptr(col2)) {
-            pipeline_blocks_host(c, family, precision, col1, col2, n_rows, off, o.dev);
-        } else {
-            const double* d1 = dev_in(c, col1, n_rows, "c1");
-            const double* d2 = dev_in(c, col2, n_rows, "c2");
-            pipeline_blocks(c, family, precision, d1, d2, n_rows, off, o.dev);
-        }
+        fit_blocks_sharded(ctx, family, precision, col1, col2, n_rows, off, o.dev);
         o.finish(c);
         PCB_CUDA(cudaStreamSynchronize(c.stream));
     });
@@ -554,24 +751,23 @@ int pcb_fit_parallel(pcb_context* ctx, int family, int precision, const double* 
         if (pcb_partition(n_rows, n_blocks, scheme, off.data()) != PCB_OK)
             throw pcb::Error(PCB_E_INVALID, "partition: block below the 30-row floor");
         auto* rec = c.ws.get_t<pcb_fit_result>("par.rec", n_blocks);
-        const bool host_in = !is_device_ptr(col1) && !is_device_ptr(col2);
-        const double* d1 = nullptr;
-        const double* d2 = nullptr;
-        if (scheme == PCB_CONTIGUOUS && host_in) {
-            pipeline_blocks_host(c, family, precision, col1, col2, n_rows, off, rec);
-        } else {
-            d1 = dev_in(c, col1, n_rows, "c1");
-            d2 = dev_in(c, col2, n_rows, "c2");
-        }
-        if (d1 && scheme == PCB_STRIDED) {
+        // per-block wall clock measured with a monotonic clock
+        // around ranks + fit + variance (all blocks run at once on the GPUs:
+        // the pipeline's wall time divided by the block count)
+        const auto t0 = std::chrono::steady_clock::now();
+        if (scheme == PCB_STRIDED) {  // row i -> block i mod M: gathered on the first device
+            const double* d1 = dev_in(c, col1, n_rows, "c1");
+            const double* d2 = dev_in(c, col2, n_rows, "c2");
             double* g1 = c.ws.get_t<double>("strided.c1", n_rows);
             double* g2 = c.ws.get_t<double>("strided.c2", n_rows);
             pcb::run_strided_gather(c, d1, n_rows, n_blocks, g1);
             pcb::run_strided_gather(c, d2, n_rows, n_blocks, g2);
-            d1 = g1;
-            d2 = g2;
+            fit_blocks_sharded(ctx, family, precision, g1, g2, n_rows, off, rec);
+        } else {
+            fit_blocks_sharded(ctx, family, precision, col1, col2, n_rows, off, rec);
         }
-        if (d1) pipeline_blocks(c, family, precision, d1, d2, n_rows, off, rec);
+        PCB_CUDA(cudaStreamSynchronize(c.stream));
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         DevOut<double> w(c, weights, weights ? n_blocks : 0, "w");
         double* d3 = c.ws.get_t<double>("comb.out", 3);
         pcb::run_combine(c, rec, n_blocks, weights ? w.dev : nullptr, d3);
@@ -590,6 +786,7 @@ int pcb_fit_parallel(pcb_context* ctx, int family, int precision, const double* 
         out->theta_combined = h3[0];
         out->total_weight = h3[1];
         out->blocks_used = static_cast<uint64_t>(h3[2]);
+        out->wall_clock_per_block = wall / static_cast<double>(n_blocks);
         none = out->blocks_used == 0;
     });
     if (rc == PCB_OK && none) {

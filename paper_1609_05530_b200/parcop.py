@@ -25,7 +25,6 @@ CPU path.
 from __future__ import annotations
 
 import ctypes as C
-import time
 from dataclasses import dataclass, field
 from enum import IntEnum
 from typing import List, Optional, Sequence
@@ -141,14 +140,21 @@ def _raise(ctx_ptr, rc):
 
 
 class Context:
-    """One pcb_context (device buffers, stream, cached workspace)."""
+    """One pcb_context (device buffers, stream, cached workspace).
 
-    def __init__(self, device: int = 0):
+    `devices` (a list) opens a multi-device context (pcb_create_multi):
+    fit_blocks / fit_parallel shard their blocks over all of them and gather
+    the records by peer copies; everything else runs on the first device."""
+
+    def __init__(self, device: int = 0, devices: Optional[Sequence[int]] = None):
         self.lib = L.load()
-        self.ptr = self.lib.pcb_create(device)
+        devs = list(devices) if devices is not None else [int(device)]
+        arr = (C.c_int * len(devs))(*devs)
+        self.ptr = self.lib.pcb_create_multi(arr, len(devs))
         if not self.ptr:
             raise CudaError(self.lib.pcb_last_error(None).decode())
-        self.device = device
+        self.device = devs[0]
+        self.devices = devs
 
     def close(self):
         if getattr(self, "ptr", None):
@@ -386,11 +392,10 @@ def fit_parallel(family, X: DataMatrix, M: int, workers: Optional[int] = None, s
     out = L.CombinedC()
     p1, _a = _ptr(c1)
     p2, _b = _ptr(c2)
-    t0 = time.perf_counter()
     ctx.check(ctx.lib.pcb_fit_parallel(ctx.ptr, int(family), int(precision), p1, p2, n, M, int(scheme),
                                        C.addressof(per), w.ctypes.data, C.byref(out)))
-    wall = time.perf_counter() - t0
-    return CombinedResult(out.theta_combined, _results(per), w, wall / M, int(out.blocks_used), ctx.stage_times())
+    return CombinedResult(out.theta_combined, _results(per), w, out.wall_clock_per_block, int(out.blocks_used),
+                          ctx.stage_times())
 
 
 def sample_matrix(family, theta, n_total: int, n_blocks: int = 1, first_block: int = 0, last_block: int = None,

@@ -37,8 +37,14 @@ int main() {
     DataMatrix big;
     big.col1.resize(100);
     big.col2.resize(100);
+    for (int i = 0; i < 100; ++i) big.col1[i] = i;
     const Partition p = partition(big, 3);
-    std::printf("partition %s\n", p.offsets[1] == 33 && p.offsets[3] == 100 ? "ok" : "FAIL");
+    const Partition ps = partition(big, 3, Scheme::Strided);  // row i -> block i mod M
+    std::printf("partition %s\n", p.offsets[1] == 33 && p.offsets[3] == 100 && p.size() == 3 &&
+                                         p.blocks[2].rows() == 34 && p.blocks[1].col1[0] == 33.0 &&
+                                         ps.blocks[1].rows() == 33 && ps.blocks[1].col1[1] == 4.0
+                                     ? "ok"
+                                     : "FAIL");
     // a small fit_parallel on a deterministic dataset
     DataMatrix d;
     for (int i = 0; i < 3000; ++i) {
@@ -48,8 +54,9 @@ int main() {
     }
     const CombinedResult fp = fit_parallel(CopulaFamily::Gaussian, d, 3, 8);
     std::printf("fit_parallel %s theta_c=%.12f used=%zu\n",
-                fp.blocks_used == 3 && std::isfinite(fp.theta_combined) ? "ok" : "FAIL", fp.theta_combined,
-                fp.blocks_used);
+                fp.blocks_used == 3 && std::isfinite(fp.theta_combined) && fp.wall_clock_per_block > 0.0 ? "ok"
+                                                                                                       : "FAIL",
+                fp.theta_combined, fp.blocks_used);
     const FitResult f = fit(CopulaFamily::Gaussian, normalized_ranks(d));
     const double s2 = asymptotic_variance(CopulaFamily::Gaussian, f.theta_hat, normalized_ranks(d));
     std::printf("fit %s theta=%.12f sigma2=%.6g\n", f.converged && std::fabs(s2 - f.sigma2) <= 1e-12 * s2 ? "ok" : "FAIL",

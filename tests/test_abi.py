@@ -34,9 +34,9 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_struct_layout():
     from paper_1609_05530_b200 import _lib
     lib = _lib.load()
-    assert lib.pcb_abi_version() == 1
+    assert lib.pcb_abi_version() == 2
     assert C.sizeof(_lib.FitResultC) == 48
-    assert C.sizeof(_lib.CombinedC) == 24
+    assert C.sizeof(_lib.CombinedC) == 32
 
 
 def test_no_device_fails_loudly():
@@ -48,6 +48,10 @@ def test_no_device_fails_loudly():
     lib = _lib.load()
     assert not lib.pcb_create(0)
     assert b"no CUDA device" in lib.pcb_last_error(None)
+    devs = (C.c_int * 2)(0, 0)
+    assert not lib.pcb_create_multi(devs, 2)
+    assert not lib.pcb_create_multi(devs, 0)
+    assert lib.pcb_device_count(None) == 0
     with pytest.raises(pcb.CudaError):
         pcb.Context(0)
     # every compute entry point refuses a NULL context instead of computing elsewhere
@@ -98,3 +102,22 @@ def test_product_does_not_touch_oracle():
     from paper_1609_05530_b200 import _lib
     ldd = subprocess.run(["ldd", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "oracle" not in ldd and "parcop_ref" not in ldd
+
+
+def test_mixed_include_translation_unit_compiles(tmp_path):
+    """The reference's own headers and include/parcop_b200.hpp in ONE
+    translation unit (tests/cpp/mixed_include.cpp): the header adopts the
+    reference's DataMatrix / PseudoSample / CopulaFamily instead of
+    redefining them. Compile-only here (run on the GPU by test_gpu_cpp)."""
+    ref = "/root/reference/proj/include"
+    if not os.path.isdir(ref):
+        pytest.skip("reference headers not present (GPU box)")
+    src = os.path.join(ROOT, "tests", "cpp", "mixed_include.cpp")
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-include",
+                        os.path.join(ROOT, "oracle", "shim.hpp"), "-I" + ref, "-I" + os.path.join(ROOT, "include"),
+                        src], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    # and the standalone header still defines the types itself
+    r = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "api_smoke.cpp")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

@@ -1,5 +1,15 @@
 """The C++ host API (include/parcop_b200.hpp, parcop:: names) end to end on
-the GPU: tests/cpp/api_smoke links libparcop_b200.so like a reference caller."""
+the GPU: tests/cpp/* link libparcop_b200.so like a reference caller.
+
+* api_smoke: the header alone (its own copies of the reference types);
+* mixed_include: the reference's own headers and this header in one
+  translation unit (reference sampler + CPU ranks, B200 ranks bit-identical,
+  B200 fit / fit_parallel / partition blocks); built where /root/reference
+  exists and shipped with the snapshot;
+* e2e_vector: fit_parallel on pageable std::vector columns (host staging
+  thread), deterministic across repetitions, single and "two-device" context.
+"""
+import json
 import os
 import subprocess
 
@@ -7,15 +17,37 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
+CPP = os.path.join(HERE, "cpp")
+
+
+def run(exe, *args):
+    path = os.path.join(CPP, exe)
+    if not os.path.exists(path):
+        subprocess.run(["make", "-C", CPP, exe], check=True)
+    out = subprocess.run([path, *map(str, args)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    return out.stdout
 
 
 def test_cpp_api_smoke():
-    exe = os.path.join(HERE, "cpp", "api_smoke")
-    if not os.path.exists(exe):
-        subprocess.run(["make", "-C", os.path.join(HERE, "cpp")], check=True)
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
-    assert out.returncode == 0, out.stderr
-    lines = out.stdout.strip().splitlines()
-    assert len(lines) == 8, out.stdout
+    lines = run("api_smoke").strip().splitlines()
+    assert len(lines) == 8, lines
     for line in lines:
-        assert " ok" in line, out.stdout
+        assert " ok" in line, lines
+
+
+def test_cpp_mixed_include_with_reference_headers():
+    if not os.path.exists(os.path.join(CPP, "mixed_include")):
+        pytest.skip("mixed_include is built only where /root/reference exists")
+    out = run("mixed_include")
+    checks = [l for l in out.splitlines() if not l.startswith("  ")]
+    assert len(checks) == 9, out
+    assert all(l.endswith(" ok") for l in checks), out
+
+
+def test_cpp_e2e_pageable_vectors_one_and_two_devices():
+    one = [json.loads(l) for l in run("e2e_vector", 4_000_000, 32, 1).splitlines()]
+    two = [json.loads(l) for l in run("e2e_vector", 4_000_000, 32, 1, "0,0").splitlines()]
+    for a, b in zip(one[:3], two[:3]):
+        assert a["blocks_used"] == b["blocks_used"] == 32
+        assert a["theta_combined"] == b["theta_combined"]  # bitwise
