@@ -528,3 +528,23 @@ def test_gumbel_near_boundary(ctx, orc, theta, seed):
     (g,) = pcb.fit_blocks(2, X, off, ctx=ctx)
     (w,) = orc.fit_blocks(2, np.asarray(X.col1), np.asarray(X.col2), off)
     check_records([g], [w], TOL64)
+
+
+# the Monte Carlo variance oracle on the device path
+# (tests/test_oracle.py runs it on the oracle): 1000 i.i.d. replicates of
+# n = 5000 (the SPEC's 200 carry ~10% sampling error), mean device sigma2
+# within 20% of the empirical variance of the device theta-hats; and the
+# 1/n scaling: sigma2 at 2n over sigma2 at n averages in [0.4, 0.6].
+@pytest.mark.parametrize("fam,theta", [(0, 0.3), (1, 5.0), (2, 2.0)])
+def test_monte_carlo_variance_oracle_device(ctx, fam, theta):
+    reps, n = 1000, 5000
+    X = pcb.sample_matrix(fam, theta, reps * n, reps, base_seed=0x5EC231, ctx=ctx)
+    off = pcb.partition(reps * n, reps).offsets
+    recs = pcb.fit_blocks(fam, X, off, ctx=ctx)
+    th = np.array([r.theta_hat for r in recs])
+    s2 = np.array([r.sigma2 for r in recs])
+    assert all(r.converged for r in recs)
+    assert 0.8 <= s2.mean() / th.var(ddof=1) <= 1.2
+    half = pcb.fit_blocks(fam, X, np.sort(np.concatenate([off, off[:-1] + n // 2])), ctx=ctx)
+    s2h = np.array([r.sigma2 for r in half]).reshape(reps, 2).mean(axis=1)
+    assert 0.4 <= np.mean(s2 / s2h) <= 0.6
