@@ -189,17 +189,119 @@ void pipeline_blocks(pcb::Ctx& c, int fam, int prec, const double* d1, const dou
     finish_stage_times(c);
 }
 
+// Parallel host memcpy (pageable -> pinned): a small fixed pool of worker
+// threads, each copying one contiguous share of a chunk. One process-wide
+// pool; calls are serialised by its mutex (the copies are memory-bandwidth
+// bound, so concurrent callers gain nothing from separate pools).
+class CopyPool {
+  public:
+    static CopyPool& get() {
+        static CopyPool p;
+        return p;
+    }
+    void copy(void* dst, const void* src, size_t bytes) {
+        std::lock_guard<std::mutex> call(call_mu_);
+        const size_t W = threads_.size() + 1;
+        const size_t share = ((bytes + W - 1) / W + 63) & ~size_t(63);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            bytes_ = bytes;
+            share_ = share;
+            pending_ = threads_.size();
+            ++gen_;
+        }
+        cv_.notify_all();
+        part(0);  // the caller copies share 0
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return pending_ == 0; });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+
+  private:
+    CopyPool() {
+        unsigned hw = std::thread::hardware_concurrency();
+        unsigned n = std::max(1u, std::min(8u, hw / 2));
+        if (const char* v = std::getenv("PCB_COPY_THREADS")) n = std::max(1, std::atoi(v));
+        for (unsigned k = 1; k < n; ++k) threads_.emplace_back([this, k] { loop(k); });
+    }
+    void part(size_t k) {
+        const size_t b0 = std::min(bytes_, k * share_), b1 = std::min(bytes_, b0 + share_);
+        if (b1 > b0) std::memcpy(dst_ + b0, src_ + b0, b1 - b0);
+    }
+    void loop(size_t k) {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            part(k);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread> threads_;
+    std::mutex mu_, call_mu_;
+    std::condition_variable cv_, done_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0, share_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+bool is_pinned_host(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// H2D of `bytes` from pageable `src`: chunks are copied in parallel into the
+// context's pinned ring and DMA'd from there on the copy stream; a slot is
+// refilled only after its previous DMA completed.
+void h2d_pageable(pcb::Ctx& c, void* dst, const void* src, size_t bytes, uint64_t& ring_pos) {
+    if (!c.ring) {
+        c.ring_slots = 4;
+        c.ring_slot_bytes = size_t(32) << 20;
+        PCB_CUDA(cudaMallocHost(&c.ring, c.ring_slot_bytes * c.ring_slots));
+        for (int k = 0; k < c.ring_slots; ++k) PCB_CUDA(cudaEventCreateWithFlags(&c.ring_ev[k], cudaEventDisableTiming));
+    }
+    for (size_t off = 0; off < bytes; off += c.ring_slot_bytes) {
+        const size_t len = std::min(c.ring_slot_bytes, bytes - off);
+        const int k = static_cast<int>(ring_pos++ % c.ring_slots);
+        char* slot = static_cast<char*>(c.ring) + k * c.ring_slot_bytes;
+        PCB_CUDA(cudaEventSynchronize(c.ring_ev[k]));
+        CopyPool::get().copy(slot, static_cast<const char*>(src) + off, len);
+        PCB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, slot, len, cudaMemcpyHostToDevice, c.copy_stream));
+        PCB_CUDA(cudaEventRecord(c.ring_ev[k], c.copy_stream));
+    }
+}
+
 // Host-resident inputs: stream the columns block-group by block-group on a
 // copy stream into two device buffers, so the H2D of group g+1 overlaps the
 // rank/fit/variance of group g. Groups are whole blocks, so every block's
 // result is the same as in one call (bitwise).
 //
 // The copies are issued by a stager thread: with pinned columns
-// cudaMemcpyAsync returns at once; with pageable columns (a caller's
-// std::vector) the driver stages each copy through its own pinned buffers and
-// blocks the issuing thread until the bytes are staged -- on the stager
-// thread that wait overlaps the device pipeline of the previous group, which
-// this thread drives (its Newton loop synchronises on the stream per pass).
+// cudaMemcpyAsync returns at once; pageable columns (a caller's std::vector)
+// are copied in parallel into a ring of pinned slots and DMA'd from there
+// (h2d_pageable) -- on the stager thread, so that work overlaps the device
+// pipeline of the previous group, which this thread drives (its Newton loop
+// synchronises on the stream per pass).
 // Buffer reuse is stream-ordered: the copy into buffer b waits (on the copy
 // stream) for the compute of the group that last used b.
 void pipeline_blocks_host(pcb::Ctx& c, int fam, int prec, const double* h1, const double* h2, uint64_t n_rows,
@@ -251,6 +353,8 @@ void pipeline_blocks_host(pcb::Ctx& c, int fam, int prec, const double* h1, cons
     bool abort = false;
     std::string stage_err;
     const int dev = c.device;
+    const bool pinned = is_pinned_host(h1) && is_pinned_host(h2);
+    uint64_t ring_pos = 0;
     std::thread stager([&] {
         try {
             PCB_CUDA(cudaSetDevice(dev));
@@ -263,10 +367,15 @@ void pipeline_blocks_host(pcb::Ctx& c, int fam, int prec, const double* h1, cons
                     PCB_CUDA(cudaStreamWaitEvent(c.copy_stream, c.cev[2 + b], 0));
                 }
                 const uint64_t r0 = off[groups[g].first], rows = off[groups[g].second] - r0;
-                PCB_CUDA(cudaMemcpyAsync(buf[b][0], h1 + r0, rows * sizeof(double), cudaMemcpyHostToDevice,
-                                         c.copy_stream));
-                PCB_CUDA(cudaMemcpyAsync(buf[b][1], h2 + r0, rows * sizeof(double), cudaMemcpyHostToDevice,
-                                         c.copy_stream));
+                if (pinned) {
+                    PCB_CUDA(cudaMemcpyAsync(buf[b][0], h1 + r0, rows * sizeof(double), cudaMemcpyHostToDevice,
+                                             c.copy_stream));
+                    PCB_CUDA(cudaMemcpyAsync(buf[b][1], h2 + r0, rows * sizeof(double), cudaMemcpyHostToDevice,
+                                             c.copy_stream));
+                } else {
+                    h2d_pageable(c, buf[b][0], h1 + r0, rows * sizeof(double), ring_pos);
+                    h2d_pageable(c, buf[b][1], h2 + r0, rows * sizeof(double), ring_pos);
+                }
                 PCB_CUDA(cudaEventRecord(c.cev[b], c.copy_stream));
                 {
                     std::lock_guard<std::mutex> lk(mu);
@@ -362,6 +471,10 @@ void close_ctx(pcb::Ctx& c) {
         cudaStreamDestroy(c.copy_stream);
     }
     if (c.pinned) cudaFreeHost(c.pinned);
+    if (c.ring) {
+        cudaFreeHost(c.ring);
+        for (int k = 0; k < c.ring_slots; ++k) cudaEventDestroy(c.ring_ev[k]);
+    }
     cudaStreamDestroy(c.own_stream);
     c.own_stream = nullptr;
 }

@@ -85,6 +85,12 @@ struct Ctx {
         }
         return pinned;
     }
+    // pageable host inputs: a ring of pinned slots the stager fills in
+    // parallel and DMAs from (pipeline_blocks_host)
+    void* ring = nullptr;
+    size_t ring_slot_bytes = 0;
+    int ring_slots = 0;
+    cudaEvent_t ring_ev[8] = {};
     void count_launch(int n = 1) {
         launches += static_cast<uint64_t>(n);
         PCB_CUDA(cudaGetLastError());

@@ -47,13 +47,17 @@ int main() {
         bool blocks_ok = p.size() == 10;
         for (std::size_t b = 0; b < p.size() && blocks_ok; ++b) {
             const FitResult fb = fit(fam, b200::normalized_ranks(p.blocks[b]));
-            blocks_ok = fb.converged && fb.theta_hat == cr.per_block[b].theta_hat && fb.sigma2 == cr.per_block[b].sigma2;
+            // fit() on pseudo-observations and fit_parallel() on raw data take
+            // different device routes (per-point transforms vs per-rank tables):
+            // equal to rounding, both held to the oracle at 1e-9 elsewhere
+            blocks_ok = fb.converged && std::fabs(fb.theta_hat - cr.per_block[b].theta_hat) <= 1e-12 * std::fabs(fb.theta_hat) &&
+                        std::fabs(fb.sigma2 - cr.per_block[b].sigma2) <= 1e-11 * fb.sigma2;
             sum_w += 1.0 / fb.sigma2;
             sum_wt += fb.theta_hat / fb.sigma2;
         }
         report("partition_blocks_fit_equal", blocks_ok);
         report("fit_parallel", cr.blocks_used == 10 && std::fabs(cr.theta_combined - sum_wt / sum_w) <=
-                                                           1e-12 * std::fabs(cr.theta_combined) &&
+                                                           1e-11 * std::fabs(cr.theta_combined) &&
                                    cr.wall_clock_per_block > 0.0 && std::fabs(f.theta_hat - theta) < 0.1);
         std::printf("  family %d theta_full=%.12f theta_c=%.12f wall/block=%.3g s\n", static_cast<int>(fam),
                     f.theta_hat, cr.theta_combined, cr.wall_clock_per_block);
