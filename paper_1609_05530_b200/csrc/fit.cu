@@ -39,6 +39,10 @@ constexpr int kMaxPasses = 64;
 constexpr double kTol64 = 1e-6;
 constexpr double kTol32 = 1e-6;
 constexpr int kWarmPasses = 2;
+#ifndef PCB_GAUSS_T_DEFAULT
+#define PCB_GAUSS_T_DEFAULT 0
+#endif
+constexpr bool kGaussT = PCB_GAUSS_T_DEFAULT != 0;
 // fp32 likelihood mode: Frank blocks whose iterate has |theta| below this run
 // the pass in fp64 per-point arithmetic (on the same fp32 edge-encoded
 // inputs). The Frank score (copula.hpp:156-172) cancels terms of size ~2/theta,
@@ -299,6 +303,7 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
                 if (gt) {
                     x = gx[j];
                     y = gy[j];
+                    if (T) T[row] = TO{static_cast<decltype(TO::x)>(x), static_cast<decltype(TO::x)>(y)};
                 } else {
                     x = dev_phi_inv(u);
                     y = dev_phi_inv(w);
@@ -831,8 +836,16 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
             goff = d_off;
         }
     }
-    void* T = (gtab && fam == kGaussian) ? nullptr
-                                         : c.ws.get("fit.T", io.n_rows * (fp32T ? sizeof(float2) : sizeof(double2)));
+    // Gaussian with rank tables: the variance pass either gathers the tables
+    // again (two random 32-byte entries per point) or streams the (x, y)
+    // pairs the prepare pass writes and recomputes exp(x^2/2) -- the same
+    // arithmetic as the table entry, so bitwise the same result
+    // (PCB_GAUSS_T=0/1 forces either way).
+    const char* gtv = std::getenv("PCB_GAUSS_T");
+    const bool gauss_t = fam == kGaussian && gtab && (gtv && gtv[0] ? gtv[0] != '0' : kGaussT);
+    void* T = (gtab && fam == kGaussian && !gauss_t)
+                  ? nullptr
+                  : c.ws.get("fit.T", io.n_rows * (fp32T ? sizeof(float2) : sizeof(double2)));
     // T32 (warm-up passes only) and the variance score zb share one 8-byte-per-row buffer.
     // Gumbel's warm-up passes read the fp64 T directly (no T32: measured faster
     // overall); PCB_WARM_FROM_T=0/1 forces either way for both families
@@ -917,7 +930,7 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
         v.u2 = io.u2;
         // Gaussian: the rank table (x, exp(x^2/2)) replaces T; Gumbel re-reads
         // T (coalesced) rather than gathering 32-byte table entries at random
-        v.gtab = fam == kGaussian ? gtab : nullptr;
+        v.gtab = (fam == kGaussian && !gauss_t) ? gtab : nullptr;
         // Frank's fp64 T is (u, v) itself; Gumbel's is (ln(-ln u), ln(-ln v))
         v.T64 = (!v.gtab && (fam == kGaussian || !fp32T)) ? static_cast<const double2*>(T) : nullptr;
         v.goff = goff;
