@@ -231,6 +231,12 @@ def run_reference(args):
                    "subsets": args.subsets, "families": [f"{n}:{t}" for n, _, t in FAMILIES]},
         "cpu_baseline": {"value": v, "unit": "points/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # the CPU arm times a bounded sample of the workload, not all of it
+        "same_config": False,
+        "bounded_sample": {"subsets_per_family": sub, "of_subsets": args.subsets, "subset_rows": args.n // args.subsets,
+                           "families": len(FAMILIES), "fit_method": "safeguarded Newton on the score root (the SPEC's "
+                           "Brent search would be 4-7x slower, SURVEY.md §0)",
+                           "projected_full_step_s": (args.n * len(FAMILIES)) / v},
     }
     print(json.dumps(line), flush=True)
 
@@ -362,14 +368,24 @@ def run_ours(args):
         l2_rate = float(json.load(open(os.path.join(ROOT, "profiles", "l2_probe.json")))["l2_random_sectors_per_s"])
     except Exception:
         l2_db, l2_rate = {}, None
+    # measured dynamic FP64 instructions per point (ncu DFMA+DADD+DMUL, profiles/r02_fp64_pipe.json):
+    # SURVEY.md §8(d) asks for the fraction by both the frozen F and the measured count
+    fp64_db = {}
+    try:
+        fp64_db = json.load(open(os.path.join(ROOT, "profiles", "r02_fp64_pipe.json")))["kernels"]
+    except Exception:
+        fp64_db = {}
     l2_sect = {}  # kernel -> sectors per step
-    per_kernel = {}  # name -> [ms, launches, bytes, fp64 instr]
-    def add(name, ms, launches, nbytes, instr, fam_name, per_launch=False):
-        e = per_kernel.setdefault(name, [0.0, 0, 0.0, 0.0])
+    per_kernel = {}  # name -> [ms, launches, bytes, fp64 instr (frozen F), fp64 instr (measured per point)]
+    def add(name, ms, launches, nbytes, instr, fam_name, per_launch=False, units=0.0):
+        e = per_kernel.setdefault(name, [0.0, 0, 0.0, 0.0, 0.0])
         e[0] += ms
         e[1] += launches
         e[2] += nbytes
         e[3] += instr
+        dyn = fp64_db.get(name, {}).get(fam_name, {}).get("fp64_instr_per_point")
+        if dyn is not None and units:
+            e[4] += dyn * units
         spp = l2_db.get(name, {}).get(fam_name) if isinstance(l2_db.get(name), dict) else None
         if spp is not None and ms > 0:
             l2_sect[name] = l2_sect.get(name, 0.0) + spp * rows * (launches if per_launch else 1)
@@ -380,19 +396,20 @@ def run_ours(args):
         add("k_prepare", st_.get("prepare", 0.0), 1, (16.0 if name == "gaussian" else 40.0) * rows, 0.0, name)
         vp = st_.get("var_point_ms", 0.0)
         # variance pass 1: read ranks + routes (+T for Gumbel); write score + two routed cross values
-        add("k_var_point", vp, 1, (64.0 if name == "gumbel" else 48.0) * rows, F_VAR[name] * rows, name)
+        add("k_var_point", vp, 1, (64.0 if name == "gumbel" else 48.0) * rows, F_VAR[name] * rows, name,
+            units=rows)
         # passes 2-3: scan reads cross + local position, writes W per slot (2 x 18 B);
         # final reads route, score, W_1, W_2 (32 B)
         add("k_var_scan+final", st_.get("variance", 0.0) - vp, 2, 68.0 * rows, 0.0, name)
         if "lik" in kernels[name]:
             lk = kernels[name]["lik"]
             add("k_lik(fp64)", lk["ms"], lk["launches"], B_PASS * rows * lk["fp64_passes"],
-                F_FIT[name] * rows * lk["fp64_passes"], name, per_launch=True)
+                F_FIT[name] * rows * lk["fp64_passes"], name, per_launch=True, units=rows * lk["fp64_passes"])
         if "warm_fp32" in kernels[name]:
             wk = kernels[name]["warm_fp32"]
             add("k_lik(fp32 warm-up)", wk["ms"], wk["launches"], 8.0 * rows * wk["launches"], 0.0, name, per_launch=True)
     table = {}
-    for kname, (kms, nl, nbytes, instr) in per_kernel.items():
+    for kname, (kms, nl, nbytes, instr, dyn) in per_kernel.items():
         if kms <= 0:
             continue
         t_hbm, t_fp64 = nbytes / hbm_peak, instr / fp64_peak
@@ -403,6 +420,12 @@ def run_ours(args):
             ach, peak, unit = instr / (kms * 1e-3) / 1e12, fp64_peak / 1e12, "T FP64-instr/s"
         table[kname] = {"ms_per_step": kms, "share": kms / ms, "launches": nl, "bound": bound, "achieved": ach,
                         "peak": peak, "unit": unit, "frac": ach / peak, "avg_launch_ms": kms / max(nl, 1)}
+        if dyn > 0:
+            table[kname]["fp64_measured"] = {
+                "instr_per_s": dyn / (kms * 1e-3), "frac": dyn / (kms * 1e-3) / fp64_peak,
+                "frac_by_frozen_F": instr / (kms * 1e-3) / fp64_peak,
+                "source": "ncu DFMA+DADD+DMUL per point (profiles/r02_fp64_pipe.json) x live ms",
+                "pipe_active_pct": {f: v.get("sm__pipe_fp64_cycles_active_pct") for f, v in fp64_db.get(kname, {}).items()}}
         if kname in l2_sect and l2_rate:
             rate = l2_sect[kname] / (kms * 1e-3)
             table[kname]["l2"] = {"sectors_per_s": rate, "peak_random_sectors_per_s": l2_rate,
