@@ -1039,6 +1039,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     // and the row finds them through route[row] = (owner, slot).
     constexpr int SB = 8;  // slice reloads in flight per thread (L2 hits)
     const uint32_t recv_sa = static_cast<uint32_t>(__cvta_generic_to_shared(recv_key));
+    uint32_t* const route_j = route + static_cast<uint64_t>(J.col) * n_rows + J.begin;
     if (tail) {
 #pragma unroll
       for (int k = 0; k < EMAX; ++k) {
@@ -1047,7 +1048,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
             const unsigned long long kk = order_key(xs[i]);
             const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
             const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
-            route[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = (d << 16) | slot;
+            route_j[i] = (d << 16) | slot;
             dsmem_st64(recv_sa + slot * 8u, d, kk);
         }
       }
@@ -1069,7 +1070,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
             const unsigned long long kk = order_key(xv[kk2]);
             const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
             const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
-            route[static_cast<uint64_t>(J.col) * n_rows + J.begin + i] = (d << 16) | slot;
+            route_j[i] = (d << 16) | slot;
             dsmem_st64(recv_sa + slot * 8u, d, kk);
         }
       }
