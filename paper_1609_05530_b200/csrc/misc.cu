@@ -272,14 +272,14 @@ __global__ void __launch_bounds__(256) k_sample(SampleTheta P, uint64_t q, uint6
         const double U0 = unit_draw(seed, 4 * i), U1 = unit_draw(seed, 4 * i + 1);
         double a, b;
         if (FAM == kGaussian) {
-            const double rr = sqrt(-2.0 * log(U0));
+            const double rr = sqrt(-2.0 * fm_log(U0));
             double sn, cs;
             sincospi(2.0 * U1, &sn, &cs);
             const double z1 = rr * cs, z2 = rr * sn;
             a = clamp_sample(0.5 * erfc(-z1 * 0x1.6a09e667f3bcdp-1));
             b = clamp_sample(0.5 * erfc(-(P.t * z1 + P.s * z2) * 0x1.6a09e667f3bcdp-1));
         } else if (FAM == kFrank) {
-            const double v = -log1p(U1 * P.d / (U1 + (1.0 - U1) * exp(-P.t * U0))) / P.t;
+            const double v = -log1p(U1 * P.d / (U1 + (1.0 - U1) * fm_exp(-P.t * U0))) / P.t;
             a = clamp_sample(U0);
             b = clamp_sample(P.t != P.s ? 1.0 - v : v);  // P.s = theta: negative theta flips v
         } else {
@@ -292,13 +292,13 @@ __global__ void __launch_bounds__(256) k_sample(SampleTheta P, uint64_t q, uint6
                 s1 = sinpi(P.al * U0);
                 s2 = sinpi(P.pal * U0);
                 s = sinpi(U0);
-                const double lw = log(-log(U1));
-                const double lf = P.c1 * (log(s2) - lw) + log(s1) - P.c2 * log(s);
-                const double l1 = log(-log(unit_draw(seed, 4 * i + 2)));
-                const double l2 = log(-log(unit_draw(seed, 4 * i + 3)));
+                const double lw = fm_log(-fm_log(U1));
+                const double lf = P.c1 * (fm_log(s2) - lw) + fm_log(s1) - P.c2 * fm_log(s);
+                const double l1 = fm_log(-fm_log(unit_draw(seed, 4 * i + 2)));
+                const double l2 = fm_log(-fm_log(unit_draw(seed, 4 * i + 3)));
                 // exp(-(e/frailty)^al) = exp(-exp(al * (log e - log frailty)))
-                a = clamp_sample(exp(-exp(P.al * (l1 - lf))));
-                b = clamp_sample(exp(-exp(P.al * (l2 - lf))));
+                a = clamp_sample(fm_exp(-fm_exp(P.al * (l1 - lf))));
+                b = clamp_sample(fm_exp(-fm_exp(P.al * (l2 - lf))));
             }
         }
         c1[r] = a;
