@@ -257,13 +257,24 @@ struct FrankTheta {
 };
 
 // score and Hessian only (the Newton pass), fp64
-__device__ __forceinline__ void frank_sh(double u, double v, const FrankTheta& f, double& s, double& h) {
-    if (f.neg) v = 1.0 - v;
+// NEG: theta < 0 (reflected); BIG: |theta| > 700 (e^{-t(hi-lo)} may leave
+// the fast exp range). Both are per block, so the Newton pass instantiates
+// the four loops and picks one per CTA.
+template <bool NEG = false, bool BIG = true>
+__device__ __forceinline__ void frank_sh_t(double u, double v, const FrankTheta& f, double& s, double& h) {
+    if (NEG) v = 1.0 - v;
     const double t = f.t;
     const bool uv = u <= v;  // inputs are finite: one compare, two selects
     const double lo = uv ? u : v, hi = uv ? v : u;
     const double ema = fm_expm1_neg(-t * (1.0 - lo));
-    const double e2 = fm_exp(-t * (hi - lo));
+    double e2;
+    if (BIG) {
+        e2 = fm_exp(-t * (hi - lo));
+    } else {
+        double sc;
+        const double p = fm_core(-t * (hi - lo), sc);
+        e2 = fma(p, sc, sc);
+    }
     const double emb = fm_expm1_neg(-t * lo);
     const double e1 = 1.0 + ema, e3 = 1.0 + emb;
     const double b = ema + e2 * emb;
@@ -273,8 +284,12 @@ __device__ __forceinline__ void frank_sh(double u, double v, const FrankTheta& f
     const double rb = fast_rcp(b);
     const double q = bp * rb;
     const double sc = f.inv_t - f.g - sum - 2.0 * q;
-    s = f.neg ? -sc : sc;
+    s = NEG ? -sc : sc;
     h = f.hconst - 2.0 * (bpp * rb - q * q);
+}
+__device__ __forceinline__ void frank_sh(double u, double v, const FrankTheta& f, double& s, double& h) {
+    if (f.neg) frank_sh_t<true, true>(u, v, f, s, h);
+    else frank_sh_t<false, true>(u, v, f, s, h);
 }
 
 // fp32 per-point arithmetic (likelihood path of configs[3]); the caller

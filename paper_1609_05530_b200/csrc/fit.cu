@@ -20,6 +20,7 @@
 #include <string>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "devmath.cuh"
@@ -422,16 +423,27 @@ __global__ void __launch_bounds__(FT, 4) k_lik(BlockState* st, const Seg* segs, 
     if constexpr (!F32) {  // fp64
         if (FAM == kFrank) {
             const FrankTheta f(theta);
+            auto pass = [&](auto neg, auto big) {
 #pragma unroll(kLikUnroll)
-            for (int k = 0; k < PPT; ++k) {
-                const uint32_t i = k * FT + threadIdx.x;
-                if (i < cnt) {
-                    const TI p = Tb[i];
-                    double s, h;
-                    frank_sh(p.x, p.y, f, s, h);
-                    v[0] += s;
-                    v[1] += h;
+                for (int k = 0; k < PPT; ++k) {
+                    const uint32_t i = k * FT + threadIdx.x;
+                    if (i < cnt) {
+                        const TI p = Tb[i];
+                        double s, h;
+                        frank_sh_t<decltype(neg)::value, decltype(big)::value>(p.x, p.y, f, s, h);
+                        v[0] += s;
+                        v[1] += h;
+                    }
                 }
+            };
+            // sign and size of theta are per block: one branch per CTA
+            const bool big = f.t > 700.0;
+            if (f.neg) {
+                if (big) pass(std::true_type{}, std::true_type{});
+                else pass(std::true_type{}, std::false_type{});
+            } else {
+                if (big) pass(std::false_type{}, std::true_type{});
+                else pass(std::false_type{}, std::false_type{});
             }
         } else {
             const GumbelTheta g(theta);

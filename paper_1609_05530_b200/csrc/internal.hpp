@@ -119,6 +119,7 @@ struct RankOut {
     uint32_t* r2s = nullptr;
     uint16_t* posl = nullptr;
     uint32_t* ocnt = nullptr;
+    unsigned long long* kside = nullptr;  // FK rank kernel: full order key per receive slot
     int cl = 0;
     uint32_t rcap = 0;
     std::vector<uint8_t> routed;  // host copy

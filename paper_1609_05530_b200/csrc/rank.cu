@@ -490,6 +490,12 @@ __device__ __forceinline__ void dsmem_st64(uint32_t saddr, uint32_t rank, unsign
     asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(ra), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void dsmem_st32(uint32_t saddr, uint32_t rank, uint32_t v) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(saddr), "r"(rank));
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
+
 // Quantile-knot map for skewed blocks (the cluster kernel's second pass):
 // kn[0..nk) sorted knot keys with kn[0] <= k, cm[j] = elements before
 // interval j (exact, cluster-wide). Interval i = [kn[i], kn[i+1]); the last
@@ -534,8 +540,13 @@ __device__ __forceinline__ uint32_t qbucket(double g, double qs, uint32_t nbtot)
 // below 0 and maps NaN to 0); monotone in the value. Senders bucket the value
 // itself, owners the received key: key_value(order_key(v)) is v (+0 for -0,
 // the same t), so both agree bit for bit.
+// t = (v/2 - hm) * scale with explicit roundings (v/2 is exact), so the
+// owner decision (cbucket_v) and the fine key of the FK kernel agree bit for bit
+__device__ __forceinline__ double cmap_t(double v, double hm, double scale) {
+    return __dmul_rn(__dsub_rn(__dmul_rn(0.5, v), hm), scale);
+}
 __device__ __forceinline__ uint32_t cbucket_v(double v, double hm, double scale, uint32_t nbtot) {
-    return min(__double2uint_rz((0.5 * v - hm) * scale), nbtot - 1u);
+    return min(__double2uint_rz(cmap_t(v, hm, scale)), nbtot - 1u);
 }
 __device__ __forceinline__ uint32_t cbucket(unsigned long long k, double hm, double scale, uint32_t nbtot) {
     return cbucket_v(key_value(k), hm, scale, nbtot);
@@ -586,14 +597,27 @@ __device__ void block_scan_excl_u16(uint32_t* cw, uint16_t* start, uint32_t n, u
 // array — the local sort keeps (bucket, index) in registers and the ranking
 // recomputes the bucket from the key; results are staged in the receive
 // buffer once the ranking is done — so a CTA needs 10 B per slot.
-template <int CTT, bool LEAN, bool QUANT = false>
+//
+// FK (opt-in variant, PCB_RANK_FK=1): owners receive 32-bit FINE keys instead of the
+// 64-bit order keys. The sender knows the global value-linear map t (the
+// owner is floor(t) >> lg_nbl), and the fine key is the position inside the
+// owner's range at 2^(32 - lg_nbl) steps per local bucket:
+// fk = sat_u32((t - owner_base) * 2^(32-lg)), exact (t has 2^-36 resolution)
+// and monotone, so the local bucket is fk's top bits and ranking compares
+// 32-bit words. Distinct values that share a fine key, and true ties, are
+// resolved from the full order keys, which the sender also writes per
+// receive slot to global memory (`kside`, L2-resident; read only for
+// equal-fine-key pairs). Halves the DSMEM bytes of the all-to-all and frees
+// shared memory for up to 4x the local buckets (NBL up to 32768). Measured
+// no faster at C5 (launch_rank_cluster), kept for the record.
+template <int CTT, bool LEAN, bool QUANT = false, bool FK = false>
 __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const ClusterJob* jobs, const double* c0, const double* c1,
                                                        uint64_t n_rows, unsigned long long* rp, uint32_t* route,
                                                        uint32_t* r2s_g, uint16_t* posl_g, uint32_t* ocnt, uint32_t K,
                                                        int32_t* fb,
                                                        int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
                                                        int tail, unsigned long long* prof, uint32_t njobs,
-                                                       uint32_t pf) {
+                                                       uint32_t pf, unsigned long long* kside) {
     namespace cg = cooperative_groups;
     constexpr int QM = LEAN ? 18 : QMAX;  // received elements per thread (RCAP <= QM * CTT)
     long long t_prev = clock64();
@@ -616,10 +640,14 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
 
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* recv_key = reinterpret_cast<unsigned long long*>(smem);
+    // FK: [fine keys, 4 B per slot | region B: the staged slice, after the send outw / lhs / perm]
+    uint32_t* const recv_fk = reinterpret_cast<uint32_t*>(smem);
+    unsigned char* const regB = smem + ((static_cast<size_t>(RCAP) * 4 + 15) & ~static_cast<size_t>(15));
     // LEAN: results staged in the receive buffer after the ranking
-    uint32_t* outw = LEAN ? reinterpret_cast<uint32_t*>(recv_key) : reinterpret_cast<uint32_t*>(recv_key + RCAP);
-    uint16_t* lhs = LEAN ? reinterpret_cast<uint16_t*>(recv_key + RCAP)
-                         : reinterpret_cast<uint16_t*>(outw + RCAP);  // NBL u16 counts -> NBL+1 starts (+1 pad)
+    uint32_t* outw = FK ? reinterpret_cast<uint32_t*>(regB)
+                        : (LEAN ? reinterpret_cast<uint32_t*>(recv_key) : reinterpret_cast<uint32_t*>(recv_key + RCAP));
+    uint16_t* lhs = (LEAN && !FK) ? reinterpret_cast<uint16_t*>(recv_key + RCAP)
+                                  : reinterpret_cast<uint16_t*>(outw + RCAP);  // NBL u16 counts -> NBL+1 starts (+1 pad)
     uint32_t* lhw = reinterpret_cast<uint32_t*>(lhs);             // the counts, two per word
     uint16_t* perm = lhs + NBL + 2;
 
@@ -632,7 +660,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     const bool staged = e > a;
     // tail mode: the slice sits after the receive buffer (where the sort's
     // arrays go later), so it stays readable while peers fill the buffer
-    unsigned char* stage_at = tail ? smem + static_cast<size_t>(RCAP) * 8 : smem;
+    unsigned char* stage_at = FK ? regB : (tail ? smem + static_cast<size_t>(RCAP) * 8 : smem);
     const double* xs = reinterpret_cast<const double*>(stage_at) + x_off - a;  // xs[i] == x[i] for i in [a, e)
     if (tid == 0 && staged) {
         const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
@@ -1040,7 +1068,24 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     constexpr int SB = 8;  // slice reloads in flight per thread (L2 hits)
     const uint32_t recv_sa = static_cast<uint32_t>(__cvta_generic_to_shared(recv_key));
     uint32_t* const route_j = route + static_cast<uint64_t>(J.col) * n_rows + J.begin;
-    if (tail) {
+    if constexpr (FK) {
+        const double P = static_cast<double>(1ull << (32 - lg_nbl));
+        unsigned long long* const kb = kside + (static_cast<uint64_t>(J.col) * K + J.seg) * CL * RCAP;
+#pragma unroll
+        for (int k = 0; k < EMAX; ++k) {
+            const uint32_t i = a + k * CTT + tid;
+            if (i < e) {
+                const double v = xs[i];
+                const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
+                const double t = cmap_t(v, hm, scale);
+                const uint32_t fk = __double2uint_rz(fma(t, P, -static_cast<double>(d << lg_nbl) * P));
+                const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
+                route_j[i] = (d << 16) | slot;
+                kb[d * RCAP + slot] = order_key(v);
+                dsmem_st32(recv_sa + slot * 4u, d, fk);
+            }
+        }
+    } else if (tail) {
 #pragma unroll
       for (int k = 0; k < EMAX; ++k) {
         const uint32_t i = a + k * CTT + tid;
@@ -1087,7 +1132,21 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     // the counting atomic's old value is the element's index inside its bucket:
     // outw[j] = bucket | index << 14 (NBL <= 16384), so the placement needs no second atomic
     uint32_t keep[QM];  // LEAN: (bucket | index) of slot tid + k*CTT, then the ranking's results
-    if constexpr (LEAN) {
+    const uint32_t fk_sh = 32 - lg_nbl;  // FK: local bucket = the fine key's top lg_nbl bits
+    if constexpr (FK) {
+        for (uint32_t j = tid; j < T; j += CTT) {
+            const uint32_t lb = recv_fk[j] >> fk_sh;
+            const uint32_t sh = (lb & 1) * 16;
+            const uint32_t idx = (atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu;
+            outw[j] = lb | (idx << 15);
+        }
+        __syncthreads();
+        block_scan_excl_u16<CTT>(lhw, lhs, NBL, s_w);
+        for (uint32_t j = tid; j < T; j += CTT) {
+            const uint32_t w = outw[j];
+            perm[lhs[w & 0x7fffu] + (w >> 15)] = static_cast<uint16_t>(j);
+        }
+    } else if constexpr (LEAN) {
 #pragma unroll
         for (int k2 = 0; k2 < QM; ++k2) {
             const uint32_t j = tid + k2 * CTT;
@@ -1142,6 +1201,43 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     //   outw = (local r2 << 16) | local sorted position | run-start bit
     // walk the elements in bucket order: a warp's lanes mostly share buckets, so
     // the bucket-mate loads are shared-memory broadcasts
+    const uint64_t reg = ((static_cast<uint64_t>(J.col) * K + J.seg) * CL + r) * RCAP;
+    if constexpr (FK) {
+#pragma unroll
+        for (int k = 0; k < QM; ++k) {
+            const uint32_t qq = tid + k * CTT;
+            if (qq >= T) break;
+            const uint32_t j = perm[qq];
+            const uint32_t fv = recv_fk[j];
+            const uint32_t lb = fv >> fk_sh;
+            const uint32_t s0 = lhs[lb], s1 = lhs[lb + 1];
+            uint32_t less = 0, eqn = 0;
+#pragma unroll 2
+            for (uint32_t q = s0; q < s1; ++q) {
+                const uint32_t f = recv_fk[perm[q]];
+                less += f < fv;
+                eqn += f == fv;
+            }
+            uint32_t same = 1, before = 0;
+            if (eqn > 1) {  // a shared fine key: the full order keys decide (ties and collisions)
+                const unsigned long long* kr = kside + reg;
+                const unsigned long long kv = __ldcg(kr + j);
+                same = 0;
+                for (uint32_t q = s0; q < s1; ++q) {
+                    const uint32_t o = perm[q];
+                    if (recv_fk[o] == fv) {
+                        const unsigned long long kq = __ldcg(kr + o);
+                        less += kq < kv;
+                        const uint32_t eq = kq == kv;
+                        same += eq;
+                        before += eq & static_cast<uint32_t>(o < j);
+                    }
+                }
+            }
+            const uint32_t llt = s0 + less;
+            outw[j] = ((2u * llt + same + 1u) << 16) | (llt + before) | (before == 0 ? 0x8000u : 0u);
+        }
+    } else
 #pragma unroll
     for (int k = 0; k < QM; ++k) {
         const uint32_t qq = tid + k * CTT;
@@ -1177,7 +1273,6 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         }
         __syncthreads();
     }
-    const uint64_t reg = ((static_cast<uint64_t>(J.col) * K + J.seg) * CL + r) * RCAP;
     if (tid == 0) ocnt[(static_cast<uint64_t>(J.col) * K + J.seg) * CL + r] = T;
     for (uint32_t j = tid; j < T; j += CTT) {  // coalesced, in slot order
         const uint32_t w = outw[j];
@@ -1189,20 +1284,52 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
 
 // quant: the quantile-knot variant, for the jobs the value-linear split could
 // not balance (fb 4 from the first launch); K = blocks (output indexing)
+// Shared memory of the FK kernel with 2^lg local buckets: fine keys (4 B per
+// slot, 16-aligned), then max(staged slice, outw + lhs + perm).
+size_t fk_smem(const ClusterPlan& p, uint32_t lg) {
+    const size_t a = (static_cast<size_t>(p.rcap) * 4 + 15) & ~static_cast<size_t>(15);
+    const size_t slice = (static_cast<size_t>(p.s) + 2) * 8 + 16;
+    const size_t sort = static_cast<size_t>(p.rcap) * 4 + ((static_cast<size_t>(1) << lg) + 2) * 2 +
+                        static_cast<size_t>(p.rcap) * 2 + 64;
+    return a + std::max(slice, sort);
+}
+
 void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, uint32_t njobs, uint32_t K,
                          const double* c0, const double* c1, uint64_t n_rows, RankOut& out, int32_t* fb,
                          int32_t* bad, bool quant = false) {
-    auto kern = p.lean ? k_rank_cluster_t<kLeanT, true>
-                       : (quant ? k_rank_cluster_t<CT, false, true> : k_rank_cluster_t<CT, false>);
+    int optin = 0;
+    PCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+    // FK kernel (32-bit fine keys; opt-in with PCB_RANK_FK=1, PCB_RANK_FK_LG
+    // local-bucket bits): measured at C5 no faster than the 64-bit-key kernel
+    // (cycles per CTA 67.6k at 2^13 buckets vs 68.0k; the send phase gains
+    // from half the DSMEM bytes less than the full-key side store costs, and
+    // 2^15 buckets make the bucket scan dominate) -- DESIGN.md, rejected variants
+    const char* fke = std::getenv("PCB_RANK_FK");
+    bool fk = !p.lean && !quant && (fke && fke[0] == '1') && out.kside != nullptr;
+    uint32_t lg_fk = 0;
+    if (fk) {
+        cudaFuncAttributes fa;
+        PCB_CUDA(cudaFuncGetAttributes(&fa, k_rank_cluster_t<CT, false, false, true>));
+        uint32_t want = std::min<uint32_t>(p.lg_nbl, 15);
+        if (const char* v = std::getenv("PCB_RANK_FK_LG")) want = static_cast<uint32_t>(std::atoi(v));
+        for (lg_fk = want; lg_fk > p.lg_nbl; --lg_fk)
+            if ((static_cast<uint64_t>(p.cl) << lg_fk) <= (1ull << 20) &&
+                fk_smem(p, lg_fk) + fa.sharedSizeBytes <= static_cast<size_t>(optin))
+                break;
+        if (lg_fk < 1 || lg_fk > 15 || fk_smem(p, lg_fk) + fa.sharedSizeBytes > static_cast<size_t>(optin)) fk = false;
+    }
+    auto kern = fk ? k_rank_cluster_t<CT, false, false, true>
+                   : (p.lean ? k_rank_cluster_t<kLeanT, true>
+                             : (quant ? k_rank_cluster_t<CT, false, true> : k_rank_cluster_t<CT, false>));
     // tail mode when the slice fits after the receive buffer (full CTAs only)
     cudaFuncAttributes fa;
     PCB_CUDA(cudaFuncGetAttributes(&fa, kern));
-    int optin = 0;
-    PCB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
     const size_t tail_bytes = static_cast<size_t>(p.rcap) * 8 + (static_cast<size_t>(p.s) + 2) * 8 + 16;
-    const int tail = (!p.lean && tail_bytes + fa.sharedSizeBytes <= static_cast<size_t>(optin) &&
-                      !getenv_flag("PCB_RANK_NO_TAIL")) ? 1 : 0;
-    const size_t smem = tail ? std::max(p.smem, tail_bytes) : p.smem;
+    const int tail = fk ? 1
+                        : ((!p.lean && tail_bytes + fa.sharedSizeBytes <= static_cast<size_t>(optin) &&
+                            !getenv_flag("PCB_RANK_NO_TAIL")) ? 1 : 0);
+    const size_t smem = fk ? fk_smem(p, lg_fk) : (tail ? std::max(p.smem, tail_bytes) : p.smem);
+    const uint32_t lg_launch = fk ? lg_fk : p.lg_nbl;
     PCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
@@ -1234,15 +1361,15 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
     }
     PCB_CUDA(cudaLaunchKernelEx(&cfg, kern, jobs, c0, c1, n_rows, out.rp, out.route, out.r2s, out.posl,
                                 out.ocnt,
-                                K, fb, bad, p.cl, p.rcap, p.lg_nbl, tail, prof, njobs, pf));
+                                K, fb, bad, p.cl, p.rcap, lg_launch, tail, prof, njobs, pf, out.kside));
     if (prof) {
         unsigned long long h[12];
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
         PCB_CUDA(cudaStreamSynchronize(c.stream));
         const double ctas = static_cast<double>(njobs) * p.cl;
-        std::fprintf(stderr, "[rank profile%s] CL=%d S=%u lean=%d: cycles/CTA  minmax %.0f  count %.0f  matrix %.0f  "
+        std::fprintf(stderr, "[rank profile%s%s] CL=%d S=%u lean=%d: cycles/CTA  minmax %.0f  count %.0f  matrix %.0f  "
                      "send %.0f  localsort %.0f  rank %.0f  qsample+sort %.0f  qhist-loop %.0f  qhist-sync %.0f  qcum %.0f  "
-                     "qshare %.0f\n", quant ? " quantile" : "", p.cl, p.s, int(p.lean), h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
+                     "qshare %.0f\n", quant ? " quantile" : "", fk ? " fk" : "", p.cl, p.s, int(p.lean), h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
                      h[4] / ctas, h[5] / ctas, h[6] / ctas, h[8] / ctas, h[9] / ctas, h[10] / ctas, h[7] / ctas);
     }
     c.count_launch();
@@ -1483,6 +1610,10 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
         out.r2s = c.ws.get_t<uint32_t>("rank.r2s", nslot);
         out.posl = c.ws.get_t<uint16_t>("rank.posl", nslot);
         out.ocnt = c.ws.get_t<uint32_t>("rank.ocnt", static_cast<size_t>(njobs) * plan.cl);
+        // full order keys per receive slot for the FK kernel's equal-fine-key
+        // resolution: shares the variance's routed cross-term buffer (same
+        // slot layout), which is written only after the ranks are consumed
+        out.kside = c.ws.get_t<unsigned long long>("var.xr", nslot);
         launch_rank_cluster(c, plan, jobs, njobs, static_cast<uint32_t>(K), d_col1, d_col2, n_rows, out, fb, d_bad);
         std::vector<int32_t> hfb(njobs);
         PCB_CUDA(cudaMemcpyAsync(hfb.data(), fb, njobs * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
