@@ -439,7 +439,7 @@ def run_ours(args):
                 "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured)" if tk["bound"] == "hbm"
                                 else "measured live: DFMA-loop microbenchmark (pcb_measure_fp64_peak)"),
                 "traffic": (traffic_db[dom] * rows if dom in traffic_db else None),
-                "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/r01_ncu_final.md, per point x points)",
+                "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/r02_ncu_full.md, per point x points)",
                 "algorithmic_bytes_per_launch": per_kernel[dom][2] / max(per_kernel[dom][1], 1),
                 "per_kernel": table}
         # SURVEY.md §8(d) pipeline roofline per GPU (B_pipe = 96 B/pt against HBM; F_pipe with the
