@@ -16,4 +16,11 @@ ncu --set full --clock-control none --import-source on \
     -k regex:'k_rank_cluster|k_var_scan|k_var_point|k_prepare|k_var_final|k_lik' -s 0 -c 14 \
     -o $O/${P}_full python bench.py --n 100000000 --subsets 800 --steps 1 --warmup 0 --no-e2e --no-cpu \
     > $O/${P}_ncu_full.log 2>&1
+# second stage (argument 2 = "parity"): C5 on every block, C4 large segments, C4 sweep, fp32 edges
+if [ "$2" = "parity" ]; then
+  python tools/parity_large.py c5 --out $O/${P}_parity_c5.json > $O/${P}_parity_c5.log 2>&1; echo "c5 rc=$?"
+  python tools/parity_large.py c4 --out $O/${P}_parity_c4.json > $O/${P}_parity_c4.log 2>&1; echo "c4 rc=$?"
+  python sweep.py --out $O/${P}_sweep_c4.jsonl > $O/${P}_sweep.log 2>&1; echo "sweep rc=$?"
+  python tools/fp32_edges.py > $O/${P}_fp32_edges.log 2>&1; tail -1 $O/${P}_fp32_edges.log
+fi
 echo done
