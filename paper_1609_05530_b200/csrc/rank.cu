@@ -1282,6 +1282,348 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     mark(5);
 }
 
+// ====================================================================
+// Two CTAs per SM (k_rank_fk2, PCB_RANK_FK2): the FK scheme (32-bit fine keys
+// over DSMEM, full order keys in the global side array `kside` for
+// equal-fine-key pairs) in a layout small enough for two co-resident CTAs of
+// 512 threads, so one CTA's barrier waits overlap the other's work. Per
+// receive slot only 6 bytes of shared memory: the fine key (4 B) and the
+// bucket-order index (2 B); the slice is not staged (the count and send
+// passes read it from global memory, the second time from L2), the counting
+// sort places with a second atomic on the same packed u16 counters (so no
+// per-slot (bucket, index) word), and the results go straight to their
+// per-slot outputs in global memory (write-combined in L2). Value-linear
+// split only: a block whose owners would overflow takes the quantile
+// relaunch of k_rank_cluster_t, exactly as from the one-per-SM kernel.
+constexpr int CT2 = 512;
+constexpr int EMAX2 = 32;  // slice elements per thread (S <= EMAX2 * CT2)
+constexpr int QM2 = 32;    // received elements per thread (RCAP <= QM2 * CT2)
+
+__global__ void __launch_bounds__(CT2, 2) k_rank_fk2(const ClusterJob* jobs, const double* c0, const double* c1,
+                                                    uint64_t n_rows, uint32_t* route, uint32_t* r2s_g,
+                                                    uint16_t* posl_g, uint32_t* ocnt, uint32_t K, int32_t* fb,
+                                                    int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
+                                                    int quant_ok, unsigned long long* prof, uint32_t njobs,
+                                                    uint32_t pf, unsigned long long* kside) {
+    namespace cg = cooperative_groups;
+    long long t_prev = clock64();
+    auto mark = [&](int k) {
+        if (prof && threadIdx.x == 0) {
+            const long long t = clock64();
+            atomicAdd(prof + k, static_cast<unsigned long long>(t - t_prev));
+            t_prev = t;
+        }
+    };
+    cg::cluster_group cluster = cg::this_cluster();
+    const int r = static_cast<int>(cluster.block_rank());
+    const uint32_t jid = blockIdx.x / CL;
+    const ClusterJob J = jobs[jid];
+    const double* x = (J.col ? c1 : c0) + J.begin;
+    const uint32_t S = slice_of(J.n, CL);
+    const uint32_t a = min(J.n, r * S), e = min(J.n, a + S);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t NBL = 1u << lg_nbl;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* const recv_fk = reinterpret_cast<uint32_t*>(smem);
+    uint16_t* const lhs = reinterpret_cast<uint16_t*>(smem + ((static_cast<size_t>(RCAP) * 4 + 15) & ~static_cast<size_t>(15)));
+    uint32_t* const lhw = reinterpret_cast<uint32_t*>(lhs);
+    uint16_t* const perm = lhs + NBL + 2;
+
+    if (tid == 32 && pf && jid + pf < njobs) {  // this CTA's slice of the job one wave ahead into L2
+        const ClusterJob J2 = jobs[jid + pf];
+        const uint32_t S2 = slice_of(J2.n, CL);
+        const uint32_t a2 = min(J2.n, r * S2), e2 = min(J2.n, a2 + S2);
+        if (e2 > a2) {
+            const double* x2 = (J2.col ? c1 : c0) + J2.begin;
+            const uint64_t p_lo = reinterpret_cast<uint64_t>(x2 + a2) & ~15ull;
+            const uint64_t p_hi = (reinterpret_cast<uint64_t>(x2 + e2) + 15ull) & ~15ull;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p_lo), "r"(static_cast<uint32_t>(p_hi - p_lo))
+                         : "memory");
+        }
+    }
+
+    __shared__ unsigned long long s_k[2][CT2 / 32];
+    __shared__ unsigned long long s_rmin, s_rmax, s_gmin, s_gmax;
+    __shared__ int s_bad, s_gbad, s_over;
+    __shared__ uint32_t s_wc[CT2 / 32][kMaxCluster];
+    __shared__ uint32_t s_cnt[kMaxCluster];
+    __shared__ uint32_t s_mat[kMaxCluster * kMaxCluster];
+    __shared__ uint32_t s_off[kMaxCluster], s_total, s_base;
+    __shared__ uint32_t s_w[CT2 / 32];
+
+    // ---- 1. bucket-map range from a strided sample (two elements per thread)
+    unsigned long long kmn = ~0ull, kmx = 0ull;
+    const uint32_t len = e - a;
+    if (len > 0) {
+        for (int h = 0; h < 2; ++h) {
+            const unsigned long long kk =
+                order_key(x[a + static_cast<uint32_t>((static_cast<uint64_t>(tid + h * CT2) * len) / (2 * CT2))]);
+            kmn = min(kmn, kk);
+            kmx = max(kmx, kk);
+        }
+    }
+    auto cta_extremes = [&]() {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+            kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+        }
+        if (lane == 0) {
+            s_k[0][wid] = kmn;
+            s_k[1][wid] = kmx;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            kmn = lane < CT2 / 32 ? s_k[0][lane] : ~0ull;
+            kmx = lane < CT2 / 32 ? s_k[1][lane] : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+                kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+            }
+            if (lane == 0) {
+                s_rmin = kmn;
+                s_rmax = kmx;
+            }
+        }
+    };
+    auto cluster_extremes = [&]() {
+        if (wid == 0) {
+            unsigned long long gmn = ~0ull, gmx = 0ull;
+            if (lane < CL) {
+                gmn = *cluster.map_shared_rank(&s_rmin, lane);
+                gmx = *cluster.map_shared_rank(&s_rmax, lane);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                gmn = min(gmn, __shfl_xor_sync(0xffffffffu, gmn, o));
+                gmx = max(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+            }
+            if (lane == 0) {
+                s_gmin = gmn;
+                s_gmax = gmx;
+            }
+        }
+        __syncthreads();
+    };
+    if (tid == 0) s_bad = 0;
+    for (int q = tid; q < (CT2 / 32) * kMaxCluster; q += CT2) (&s_wc[0][0])[q] = 0u;
+    cta_extremes();
+    cluster.sync();
+    mark(0);
+    cluster_extremes();
+    if (s_gmin == s_gmax) {  // exact extremes over every element (constant-looking sample)
+        kmn = ~0ull;
+        kmx = 0ull;
+        for (uint32_t i = a + tid; i < e; i += CT2) {
+            const unsigned long long kk = order_key(x[i]);
+            kmn = min(kmn, kk);
+            kmx = max(kmx, kk);
+        }
+        __syncthreads();
+        cluster.sync();
+        cta_extremes();
+        cluster.sync();
+        cluster_extremes();
+    }
+    const double vmin = key_value(s_gmin), vmax = key_value(s_gmax);
+    const double hm = 0.5 * vmin;
+    const uint32_t nbtot = static_cast<uint32_t>(CL) << lg_nbl;
+    const double scale = static_cast<double>(nbtot) / (0.5 * vmax - hm);
+    const bool constant = s_gmin == s_gmax;
+    if (constant || !(isfinite(scale) && scale > 0.0 && isfinite(hm))) {
+        if (constant && !isfinite(vmin)) {
+            if (r == 0 && tid == 0) {
+                bad[J.seg] = 1;
+                fb[jid] = 2;
+            }
+        } else if (constant) {
+            if (r == 0 && tid == 0) fb[jid] = 3;
+        } else if (r == 0 && tid == 0) {
+            fb[jid] = 1;
+        }
+        cluster.sync();
+        return;
+    }
+
+    // ---- 2. owners and per-warp counts (the slice from global memory)
+    uint32_t bk[EMAX2 / 8];
+#pragma unroll
+    for (int k = 0; k < EMAX2 / 8; ++k) bk[k] = 0u;
+    bool fin = true;
+#pragma unroll
+    for (int h = 0; h < EMAX2 / 8; ++h) {  // 8 loads in flight per thread
+        if (a + h * 8 * CT2 >= e) break;
+        double xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = a + (h * 8 + u) * CT2 + tid;
+            xv[u] = i < e ? __ldg(x + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t i = a + (h * 8 + u) * CT2 + tid;
+            if (i < e) {
+                fin &= isfinite(xv[u]);
+                bk[h] |= (cbucket_v(xv[u], hm, scale, nbtot) >> lg_nbl) << (u * 4);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < EMAX2; ++k)
+        if (a + k * CT2 + tid < e) atomicAdd(&s_wc[wid][(bk[k >> 3] >> ((k & 7) * 4)) & 0xfu], 1u);
+    if (!__syncthreads_and(fin) && tid == 0) s_bad = 1;
+    if (tid < CL) {
+        uint32_t run = 0;
+        for (int w = 0; w < CT2 / 32; ++w) {
+            const uint32_t c = s_wc[w][tid];
+            s_wc[w][tid] = run;
+            run += c;
+        }
+        s_cnt[tid] = run;
+    }
+    cluster.sync();
+    mark(1);
+    if (tid < CL * CL) s_mat[tid] = *cluster.map_shared_rank(&s_cnt[tid % CL], tid / CL);
+    if (wid == 1) {
+        const int gb = __any_sync(0xffffffffu, lane < CL && *cluster.map_shared_rank(&s_bad, lane) != 0);
+        if (lane == 0) s_gbad = gb;
+    }
+    __syncthreads();
+    if (s_gbad) {
+        if (r == 0 && tid == 0) {
+            bad[J.seg] = 1;
+            fb[jid] = 2;
+        }
+        cluster.sync();
+        return;
+    }
+    if (wid == 0) {
+        uint32_t col = 0, mine = 0;
+        if (lane < CL)
+            for (int q = 0; q < CL; ++q) {
+                const uint32_t v = s_mat[q * CL + lane];
+                col += v;
+                if (q < r) mine += v;
+            }
+        if (lane < CL) s_off[lane] = mine;
+        const bool over = __any_sync(0xffffffffu, lane < CL && col > RCAP);
+        uint32_t below = lane < r ? col : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+        const uint32_t total = __shfl_sync(0xffffffffu, col, r);
+        if (lane == 0) {
+            s_total = total;
+            s_base = below;
+            s_over = over;
+        }
+    }
+    __syncthreads();
+    if (s_over) {
+        if (r == 0 && tid == 0) fb[jid] = quant_ok ? 4 : 1;
+        cluster.sync();
+        return;
+    }
+    for (int q = tid; q < (CT2 / 32) * CL; q += CT2) s_wc[q / CL][q % CL] += s_off[q % CL];
+    __syncthreads();
+
+    // ---- 3. send: fine key over DSMEM, full key to the side array, route per row
+    const uint32_t recv_sa = static_cast<uint32_t>(__cvta_generic_to_shared(recv_fk));
+    uint32_t* const route_j = route + static_cast<uint64_t>(J.col) * n_rows + J.begin;
+    const uint64_t reg0 = (static_cast<uint64_t>(J.col) * K + J.seg) * CL;
+    {
+        const double P = static_cast<double>(1ull << (32 - lg_nbl));
+        unsigned long long* const kb = kside + reg0 * RCAP;
+#pragma unroll
+        for (int h = 0; h < EMAX2 / 8; ++h) {
+            if (a + h * 8 * CT2 >= e) break;
+            double xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = a + (h * 8 + u) * CT2 + tid;
+                xv[u] = i < e ? __ldcg(x + i) : 0.0;  // second read of the slice: L2
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = a + (h * 8 + u) * CT2 + tid;
+                if (i < e) {
+                    const double v = xv[u];
+                    const uint32_t d = (bk[h] >> (u * 4)) & 0xfu;
+                    const double t = cmap_t(v, hm, scale);
+                    const uint32_t fk = __double2uint_rz(fma(t, P, -static_cast<double>(d << lg_nbl) * P));
+                    const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
+                    route_j[i] = (d << 16) | slot;
+                    kb[d * RCAP + slot] = order_key(v);
+                    dsmem_st32(recv_sa + slot * 4u, d, fk);
+                }
+            }
+        }
+    }
+    cluster.sync();  // every receive buffer is complete; no DSMEM access after this point
+    mark(3);
+
+    // ---- 4. counting sort into NBL local buckets (the fine key's top bits):
+    // count, scan to starts, then place with a second atomic on the same
+    // packed counters (afterwards lhs[b] = end of bucket b)
+    const uint32_t T = s_total, base = s_base;
+    const uint32_t fk_sh = 32 - lg_nbl;
+    for (uint32_t q = tid; q <= NBL / 2; q += CT2) lhw[q] = 0u;
+    __syncthreads();
+    for (uint32_t j = tid; j < T; j += CT2) {
+        const uint32_t lb = recv_fk[j] >> fk_sh;
+        atomicAdd(lhw + (lb >> 1), 1u << ((lb & 1) * 16));
+    }
+    __syncthreads();
+    block_scan_excl_u16<CT2>(lhw, lhs, NBL, s_w);
+    for (uint32_t j = tid; j < T; j += CT2) {
+        const uint32_t lb = recv_fk[j] >> fk_sh, sh = (lb & 1) * 16;
+        perm[(atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu] = static_cast<uint16_t>(j);
+    }
+    __syncthreads();
+    mark(4);
+
+    // ---- 5. rank inside each bucket; results straight to the per-slot outputs
+    const uint64_t reg = (reg0 + r) * RCAP;
+    const unsigned long long* const kr = kside + reg;
+#pragma unroll 1
+    for (int k = 0; k < QM2; ++k) {
+        const uint32_t qq = tid + k * CT2;
+        if (qq >= T) break;
+        const uint32_t j = perm[qq];
+        const uint32_t fv = recv_fk[j];
+        const uint32_t lb = fv >> fk_sh;
+        const uint32_t s0 = lb ? lhs[lb - 1] : 0u, s1 = lhs[lb];
+        uint32_t less = 0, eqn = 0;
+#pragma unroll 2
+        for (uint32_t q = s0; q < s1; ++q) {
+            const uint32_t f = recv_fk[perm[q]];
+            less += f < fv;
+            eqn += f == fv;
+        }
+        uint32_t same = 1, before = 0;
+        if (eqn > 1) {  // a shared fine key: the full order keys decide (ties and collisions)
+            const unsigned long long kv = __ldcg(kr + j);
+            same = 0;
+            for (uint32_t q = s0; q < s1; ++q) {
+                const uint32_t o = perm[q];
+                if (recv_fk[o] == fv) {
+                    const unsigned long long kq = __ldcg(kr + o);
+                    less += kq < kv;
+                    const uint32_t eq = kq == kv;
+                    same += eq;
+                    before += eq & static_cast<uint32_t>(o < j);
+                }
+            }
+        }
+        const uint32_t llt = s0 + less;
+        r2s_g[reg + j] = 2u * base + 2u * llt + same + 1u;
+        posl_g[reg + j] = static_cast<uint16_t>((llt + before) | (before == 0 ? 0x8000u : 0u));
+    }
+    if (tid == 0) ocnt[reg0 + r] = T;
+    mark(5);
+}
+
 // quant: the quantile-knot variant, for the jobs the value-linear split could
 // not balance (fb 4 from the first launch); K = blocks (output indexing)
 // Shared memory of the FK kernel with 2^lg local buckets: fine keys (4 B per
@@ -1317,6 +1659,66 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
                 fk_smem(p, lg_fk) + fa.sharedSizeBytes <= static_cast<size_t>(optin))
                 break;
         if (lg_fk < 1 || lg_fk > 15 || fk_smem(p, lg_fk) + fa.sharedSizeBytes > static_cast<size_t>(optin)) fk = false;
+    }
+    // two-CTAs-per-SM fine-key kernel (PCB_RANK_FK2=1)
+    const char* fk2e = std::getenv("PCB_RANK_FK2");
+    if (!p.lean && !quant && out.kside != nullptr && fk2e && fk2e[0] == '1' &&
+        p.rcap <= static_cast<uint32_t>(QM2 * CT2) && p.s <= static_cast<uint32_t>(EMAX2 * CT2) && p.lg_nbl <= 15) {
+        const size_t smem2 = ((static_cast<size_t>(p.rcap) * 4 + 15) & ~static_cast<size_t>(15)) +
+                             ((static_cast<size_t>(1) << p.lg_nbl) + 2) * 2 + static_cast<size_t>(p.rcap) * 2 + 64;
+        PCB_CUDA(cudaFuncSetAttribute(k_rank_fk2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2)));
+        if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(k_rank_fk2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        int per_sm = 0;
+        PCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rank_fk2, CT2, smem2));
+        if (per_sm >= 2) {
+            // would the quantile relaunch (one-per-SM kernel, tail mode) have room for its tables?
+            cudaFuncAttributes fq;
+            PCB_CUDA(cudaFuncGetAttributes(&fq, k_rank_cluster_t<CT, false, true>));
+            const size_t tb = static_cast<size_t>(p.rcap) * 8 + (static_cast<size_t>(p.s) + 2) * 8 + 16;
+            const uint32_t subslots = (128 + 128 / 16) + (128 / 2 + 1) + 128;
+            const int quant_ok = (tb + fq.sharedSizeBytes <= static_cast<size_t>(optin) &&
+                                  p.rcap >= 3200 + (p.s + 3) / 4 + subslots) ? 1 : 0;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(njobs * static_cast<uint32_t>(p.cl));
+            cfg.blockDim = dim3(CT2);
+            cfg.dynamicSmemBytes = smem2;
+            cfg.stream = c.stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = static_cast<unsigned>(p.cl);
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            uint32_t pf = 0;
+            if (const char* e = std::getenv("PCB_RANK_PF")) {
+                pf = static_cast<uint32_t>(std::atoi(e));
+            } else {
+                int ncl = 0;
+                if (cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void*>(k_rank_fk2), &cfg) == cudaSuccess &&
+                    ncl > 0)
+                    pf = static_cast<uint32_t>(ncl);
+                cudaGetLastError();
+            }
+            unsigned long long* prof = nullptr;
+            if (getenv_flag("PCB_RANK_PROFILE")) {
+                prof = c.ws.get_t<unsigned long long>("rank.prof", 12);
+                PCB_CUDA(cudaMemsetAsync(prof, 0, 12 * sizeof(unsigned long long), c.stream));
+            }
+            PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_fk2, jobs, c0, c1, n_rows, out.route, out.r2s, out.posl, out.ocnt,
+                                        K, fb, bad, p.cl, p.rcap, p.lg_nbl, quant_ok, prof, njobs, pf, out.kside));
+            if (prof) {
+                unsigned long long h[12];
+                PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+                PCB_CUDA(cudaStreamSynchronize(c.stream));
+                const double ctas = static_cast<double>(njobs) * p.cl;
+                std::fprintf(stderr, "[rank profile fk2] CL=%d S=%u (2 CTAs/SM): cycles/CTA  minmax %.0f  count %.0f  "
+                             "send %.0f  localsort %.0f  rank %.0f\n", p.cl, p.s, h[0] / ctas, h[1] / ctas, h[3] / ctas,
+                             h[4] / ctas, h[5] / ctas);
+            }
+            c.count_launch();
+            return;
+        }
     }
     auto kern = fk ? k_rank_cluster_t<CT, false, false, true>
                    : (p.lean ? k_rank_cluster_t<kLeanT, true>
