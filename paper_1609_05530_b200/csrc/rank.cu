@@ -1660,7 +1660,7 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
                 break;
         if (lg_fk < 1 || lg_fk > 15 || fk_smem(p, lg_fk) + fa.sharedSizeBytes > static_cast<size_t>(optin)) fk = false;
     }
-    // two-CTAs-per-SM fine-key kernel (PCB_RANK_FK2=1)
+    // two-CTAs-per-SM fine-key kernel (opt-in PCB_RANK_FK2=1; measured 41% slower at C5)
     const char* fk2e = std::getenv("PCB_RANK_FK2");
     if (!p.lean && !quant && out.kside != nullptr && fk2e && fk2e[0] == '1' &&
         p.rcap <= static_cast<uint32_t>(QM2 * CT2) && p.s <= static_cast<uint32_t>(EMAX2 * CT2) && p.lg_nbl <= 15) {

@@ -403,6 +403,34 @@ def test_rank_lean_variant_identical(ctx, orc, env):
     assert abs(r.theta_hat - w.theta_hat) <= 1e-9 * w.theta_hat and abs(r.sigma2 - w.sigma2) <= 1e-9 * w.sigma2
 
 
+@pytest.mark.parametrize("var", ["PCB_RANK_FK", "PCB_RANK_FK2"])
+def test_rank_fine_key_variants_identical(ctx, orc, env, var):
+    """The fine-key rank kernels (32-bit keys over DSMEM, full keys in the
+    side array for equal fine keys; FK2: two CTAs per SM) rank bit-identically
+    on continuous, tie-heavy, signed-zero and skewed columns, and feed the same fit."""
+    rng = np.random.default_rng(17)
+    n = 375000
+    z = rng.standard_normal(n)
+    c2 = np.round(rng.uniform(size=n), 3)
+    c2[::97] = -0.0
+    c2[1::97] = 0.0
+    X = pcb.DataMatrix(rng.uniform(size=n), c2)
+    off = np.linspace(0, n, 4).astype(np.uint64)
+    a = pcb.normalized_ranks(X, off, ctx=ctx)
+    S = pcb.DataMatrix(z, np.exp(2.0 * z))  # skewed: overflowing owners take the quantile relaunch
+    sa = pcb.normalized_ranks(S, off, ctx=ctx)
+    env.setenv(var, "1")
+    b = pcb.normalized_ranks(X, off, ctx=ctx)
+    sb = pcb.normalized_ranks(S, off, ctx=ctx)
+    assert np.array_equal(a.u1, b.u1) and np.array_equal(a.u2, b.u2)
+    assert np.array_equal(sa.u1, sb.u1) and np.array_equal(sa.u2, sb.u2)
+    assert np.array_equal(b.u2, oracle_ranks(orc, X.col2, off))
+    Y = pcb.sample_matrix(1, 5.0, 250000, 2, ctx=ctx)
+    r = pcb.fit_blocks(1, Y, [0, 125000, 250000], ctx=ctx)
+    w = orc.fit_blocks(1, np.asarray(Y.col1), np.asarray(Y.col2), np.array([0, 125000, 250000], np.uint64))
+    check_records(r, w, TOL64)
+
+
 @pytest.mark.parametrize("fam,theta", FAMS)
 def test_variance_cluster_vs_global(ctx, orc, env, fam, theta):
     n, k = 60000, 3
