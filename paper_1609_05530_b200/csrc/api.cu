@@ -174,15 +174,6 @@ void pipeline_blocks(pcb::Ctx& c, int fam, int prec, const double* d1, const dou
     const uint64_t K = off.size() - 1;
     RankBufs rb = rank_buffers(c, n_rows, K);
     PCB_CUDA(cudaEventRecord(c.ev[0], c.stream));
-    // slot tables: the rank kernel writes each receive slot's rank-table entry,
-    // so prepare / variance gather one word per column (PCB_SLOT_TAB=0: off)
-    const char* stv = std::getenv("PCB_SLOT_TAB");
-    if (fam != PCB_FRANK && !(stv && stv[0] == '0')) {  // Gaussian and Gumbel
-        const pcb::RankTables t = pcb::rank_tables(c, fam, off);
-        rb.r.stab = t.tab;
-        rb.r.sgoff = t.goff;
-        rb.r.sfam = fam;
-    }
     pcb::run_ranks(c, d1, d2, n_rows, off, rb.r, rb.bad);
     pcb::FitIO io;
     io.family = fam;

@@ -153,9 +153,6 @@ struct RankRef {
     const uint32_t* r2s;           // [2][nseg][cl][rcap] r2 per slot
     const uint8_t* routed;         // [nseg] or null
     uint32_t cl, rcap;
-    // per receive slot, the rank table entry of its r2 (Gaussian: (Phi^-1(u), exp(x^2/2));
-    // Gumbel: (ln(-ln u), u)), written by the rank kernel; null when absent
-    const double2* sx;
 };
 
 __device__ __forceinline__ uint64_t slot_index(const RankRef& R, int nseg, int col, int m, uint32_t rw) {

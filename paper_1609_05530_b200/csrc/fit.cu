@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
 #endif
     constexpr int U = FAM == kGumbel ? PCB_U_PREP_U : PCB_U_PREP;  // points per thread in flight (measured at C5)
     for (int k0 = 0; k0 < PPT; k0 += U) {
-        double uu[U], ww[U], gx[U], gy[U];  // (uu, ww: Gaussian via slot tables: unused)
+        double uu[U], ww[U], gx[U], gy[U];
         uint32_t ra[U], rb[U];
         if (!u1) {
 #pragma unroll
@@ -263,20 +263,7 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
                     }
                 }
             }
-            if (rt && R.sx && FAM != kFrank) {  // slot tables: one gather per column
-#pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
-                    if (i < S.n) {
-                        const double2 a2 = R.sx[slot_index(R, nseg, 0, m, ra[j])];
-                        const double2 b2 = R.sx[slot_index(R, nseg, 1, m, rb[j])];
-                        gx[j] = a2.x;
-                        gy[j] = b2.x;
-                        uu[j] = a2.y;  // Gumbel: u itself (Gaussian: exp(x^2/2), unused here)
-                        ww[j] = b2.y;
-                    }
-                }
-            } else if (rt) {
+            if (rt) {
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
                     const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
@@ -287,7 +274,6 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
                 }
             }
         }
-        const bool via_sx = !u1 && rt && R.sx && FAM != kFrank;
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
@@ -296,8 +282,6 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
                 if (u1) {
                     uu[j] = u1[row];
                     ww[j] = u2[row];
-                } else if (via_sx) {
-                    // gx, gy, uu, ww already hold the slot-table entries
                 } else {
                     const uint32_t r1 = ra[j], r2 = rb[j];
                     uu[j] = __dmul_rn(0.5 * static_cast<double>(r1), scale);
@@ -800,39 +784,6 @@ std::vector<Seg> make_segs(const std::vector<uint64_t>& off, uint32_t& tiles) {
 
 }  // namespace
 
-RankTables rank_tables(Ctx& c, int fam, const std::vector<uint64_t>& off) {
-    RankTables t;
-    if (!(fam == kGaussian || fam == kGumbel) || getenv_flag("PCB_NO_GTAB")) return t;
-    const int K = static_cast<int>(off.size() - 1);
-    std::vector<uint32_t> sizes;
-    for (int m = 0; m < K; ++m) {
-        const uint32_t n = static_cast<uint32_t>(off[m + 1] - off[m]);
-        if (std::find(sizes.begin(), sizes.end(), n) == sizes.end()) sizes.push_back(n);
-    }
-    if (sizes.size() > 16) return t;
-    std::vector<uint64_t> base(sizes.size());
-    uint64_t tot = 0;
-    for (size_t q = 0; q < sizes.size(); ++q) {
-        base[q] = tot;
-        tot += 2ull * sizes[q] + 1;
-    }
-    auto* tab = c.ws.get_t<double>("fit.gtab", 4 * tot);  // 4 doubles per entry
-    std::vector<uint64_t> hoff(K);
-    for (int m = 0; m < K; ++m)
-        hoff[m] = base[std::find(sizes.begin(), sizes.end(), static_cast<uint32_t>(off[m + 1] - off[m])) - sizes.begin()];
-    auto* d_off = c.ws.get_t<uint64_t>("fit.goff", K);
-    PCB_CUDA(cudaMemcpyAsync(d_off, hoff.data(), K * sizeof(uint64_t), cudaMemcpyHostToDevice, c.stream));
-    for (size_t q = 0; q < sizes.size(); ++q) {
-        const uint32_t nn = sizes[q];
-        k_rank_table<<<std::min<uint32_t>(148u * 8u, (2 * nn + 256) / 256), 256, 0, c.stream>>>(tab + 4 * base[q], nn,
-                                                                                                fam);
-        c.count_launch();
-    }
-    t.tab = tab;
-    t.goff = d_off;
-    return t;
-}
-
 void init_tables() {
     build_tables();
     PCB_CUDA(cudaMemcpyToSymbol(c_frank_rho, h_frank_rho, sizeof h_frank_rho));
@@ -870,14 +821,31 @@ void run_fit(Ctx& c, const FitIO& io, void* d_out) {
     // Gaussian scores by rank table (rank-derived u only; few distinct block sizes)
     const double* gtab = nullptr;
     const uint64_t* goff = nullptr;
-    if ((fam == kGaussian || fam == kGumbel) && !io.u1) {
-        if (io.rank && io.rank->stab) {  // built before the rank stage (slot tables)
-            gtab = io.rank->stab;
-            goff = io.rank->sgoff;
-        } else {
-            const RankTables t = rank_tables(c, fam, io.off);
-            gtab = t.tab;
-            goff = t.goff;
+    if ((fam == kGaussian || fam == kGumbel) && !io.u1 && !getenv_flag("PCB_NO_GTAB")) {
+        std::vector<uint32_t> sizes;
+        for (int m = 0; m < K; ++m)
+            if (std::find(sizes.begin(), sizes.end(), segs[m].n) == sizes.end()) sizes.push_back(segs[m].n);
+        if (sizes.size() <= 16) {
+            std::vector<uint64_t> base(sizes.size());
+            uint64_t tot = 0;
+            for (size_t q = 0; q < sizes.size(); ++q) {
+                base[q] = tot;
+                tot += 2ull * sizes[q] + 1;
+            }
+            auto* tab = c.ws.get_t<double>("fit.gtab", 4 * tot);  // 4 doubles per entry
+            std::vector<uint64_t> hoff(K);
+            for (int m = 0; m < K; ++m)
+                hoff[m] = base[std::find(sizes.begin(), sizes.end(), segs[m].n) - sizes.begin()];
+            auto* d_off = c.ws.get_t<uint64_t>("fit.goff", K);
+            PCB_CUDA(cudaMemcpyAsync(d_off, hoff.data(), K * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+            for (size_t q = 0; q < sizes.size(); ++q) {
+                const uint32_t nn = sizes[q];
+                k_rank_table<<<std::min<uint32_t>(148u * 8u, (2 * nn + 256) / 256), 256, 0, s>>>(tab + 4 * base[q], nn,
+                                                                                                   fam);
+                c.count_launch();
+            }
+            gtab = tab;
+            goff = d_off;
         }
     }
     // Gaussian with rank tables: the variance pass either gathers the tables

@@ -120,18 +120,12 @@ struct RankOut {
     uint16_t* posl = nullptr;
     uint32_t* ocnt = nullptr;
     unsigned long long* kside = nullptr;  // FK rank kernel: full order key per receive slot
-    // slot tables: when stab is set (raw-data pipelines, Gaussian / Gumbel),
-    // the rank kernels write sx[slot] = the rank table entry of the slot's r2
-    const double* stab = nullptr;
-    const uint64_t* sgoff = nullptr;  // per block: offset of its size's table (entries)
-    int sfam = -1;
-    double2* sx = nullptr;
     int cl = 0;
     uint32_t rcap = 0;
     std::vector<uint8_t> routed;  // host copy
     uint8_t* d_routed = nullptr;  // device copy
     RankRef ref() const {
-        return RankRef{rp, route, r2s, d_routed, static_cast<uint32_t>(cl), rcap, sx};
+        return RankRef{rp, route, r2s, d_routed, static_cast<uint32_t>(cl), rcap};
     }
 };
 
@@ -163,15 +157,6 @@ struct FitIO {
     bool do_fit = true;
     bool do_variance = true;
 };
-
-// Per-block-size rank tables (k_rank_table): 32-byte entries by r2 for the
-// Gaussian {Phi^-1(u), exp(x^2/2), 0, 0} and Gumbel {ln(-ln u), -ln u, 1/(-ln u), 1/u};
-// tab == nullptr when not used (Frank, > 16 distinct sizes, PCB_NO_GTAB).
-struct RankTables {
-    const double* tab = nullptr;
-    const uint64_t* goff = nullptr;  // device, per block: first entry of its size's table
-};
-RankTables rank_tables(Ctx& c, int fam, const std::vector<uint64_t>& off);
 
 // Runs prepare -> init -> Newton passes -> variance; writes n_seg
 // pcb_fit_result-compatible records (device) into d_out.

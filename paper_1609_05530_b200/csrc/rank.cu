@@ -496,17 +496,6 @@ __device__ __forceinline__ void dsmem_st32(uint32_t saddr, uint32_t rank, uint32
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
 }
 
-// Slot-table entry of rank r2 (the consumers' per-rank transform, fetched
-// once per slot here so prepare / variance gather one 16-byte word per
-// column instead of r2 and then the table): Gaussian (Phi^-1(u), exp(x^2/2)),
-// Gumbel (ln(-ln u), u) with u = clamp_unit((r2/2) * (1/(n+1))) exactly as
-// the prepare pass computes it.
-__device__ __forceinline__ double2 slot_entry(const double* tab, uint32_t r2, int fam, double scale) {
-    const double* e = tab + 4 * static_cast<uint64_t>(r2);
-    if (fam == kGaussian) return make_double2(e[0], e[1]);
-    return make_double2(e[0], fmin(fmax(__dmul_rn(0.5 * static_cast<double>(r2), scale), 1e-12), 1.0 - 1e-12));
-}
-
 // Quantile-knot map for skewed blocks (the cluster kernel's second pass):
 // kn[0..nk) sorted knot keys with kn[0] <= k, cm[j] = elements before
 // interval j (exact, cluster-wide). Interval i = [kn[i], kn[i+1]); the last
@@ -628,8 +617,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
                                                        int32_t* fb,
                                                        int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
                                                        int tail, unsigned long long* prof, uint32_t njobs,
-                                                       uint32_t pf, unsigned long long* kside, const double* stab,
-                                                       const uint64_t* sgoff, double2* sx, int sfam) {
+                                                       uint32_t pf, unsigned long long* kside) {
     namespace cg = cooperative_groups;
     constexpr int QM = LEAN ? 18 : QMAX;  // received elements per thread (RCAP <= QM * CTT)
     long long t_prev = clock64();
@@ -1286,14 +1274,10 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         __syncthreads();
     }
     if (tid == 0) ocnt[(static_cast<uint64_t>(J.col) * K + J.seg) * CL + r] = T;
-    const double* const st_m = sx ? stab + 4 * sgoff[J.seg] : nullptr;
-    const double sscale = 1.0 / (static_cast<double>(J.n) + 1.0);
     for (uint32_t j = tid; j < T; j += CTT) {  // coalesced, in slot order
         const uint32_t w = outw[j];
-        const uint32_t r2 = 2u * base + (w >> 16);
-        r2s_g[reg + j] = r2;
+        r2s_g[reg + j] = 2u * base + (w >> 16);
         posl_g[reg + j] = static_cast<uint16_t>(w & 0xffffu);
-        if (st_m) sx[reg + j] = slot_entry(st_m, r2, sfam, sscale);
     }
     mark(5);
 }
@@ -1320,8 +1304,7 @@ __global__ void __launch_bounds__(CT2, 2) k_rank_fk2(const ClusterJob* jobs, con
                                                     uint16_t* posl_g, uint32_t* ocnt, uint32_t K, int32_t* fb,
                                                     int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
                                                     int quant_ok, unsigned long long* prof, uint32_t njobs,
-                                                    uint32_t pf, unsigned long long* kside, const double* stab,
-                                                    const uint64_t* sgoff, double2* sx, int sfam) {
+                                                    uint32_t pf, unsigned long long* kside) {
     namespace cg = cooperative_groups;
     long long t_prev = clock64();
     auto mark = [&](int k) {
@@ -1634,10 +1617,8 @@ __global__ void __launch_bounds__(CT2, 2) k_rank_fk2(const ClusterJob* jobs, con
             }
         }
         const uint32_t llt = s0 + less;
-        const uint32_t r2 = 2u * base + 2u * llt + same + 1u;
-        r2s_g[reg + j] = r2;
+        r2s_g[reg + j] = 2u * base + 2u * llt + same + 1u;
         posl_g[reg + j] = static_cast<uint16_t>((llt + before) | (before == 0 ? 0x8000u : 0u));
-        if (sx) sx[reg + j] = slot_entry(stab + 4 * sgoff[J.seg], r2, sfam, 1.0 / (static_cast<double>(J.n) + 1.0));
     }
     if (tid == 0) ocnt[reg0 + r] = T;
     mark(5);
@@ -1725,8 +1706,7 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
                 PCB_CUDA(cudaMemsetAsync(prof, 0, 12 * sizeof(unsigned long long), c.stream));
             }
             PCB_CUDA(cudaLaunchKernelEx(&cfg, k_rank_fk2, jobs, c0, c1, n_rows, out.route, out.r2s, out.posl, out.ocnt,
-                                        K, fb, bad, p.cl, p.rcap, p.lg_nbl, quant_ok, prof, njobs, pf, out.kside,
-                                        out.stab, out.sgoff, out.sx, out.sfam));
+                                        K, fb, bad, p.cl, p.rcap, p.lg_nbl, quant_ok, prof, njobs, pf, out.kside));
             if (prof) {
                 unsigned long long h[12];
                 PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
@@ -1783,8 +1763,7 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
     }
     PCB_CUDA(cudaLaunchKernelEx(&cfg, kern, jobs, c0, c1, n_rows, out.rp, out.route, out.r2s, out.posl,
                                 out.ocnt,
-                                K, fb, bad, p.cl, p.rcap, lg_launch, tail, prof, njobs, pf, out.kside, out.stab,
-                                out.sgoff, out.sx, out.sfam));
+                                K, fb, bad, p.cl, p.rcap, lg_launch, tail, prof, njobs, pf, out.kside));
     if (prof) {
         unsigned long long h[12];
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
@@ -2037,7 +2016,6 @@ void run_ranks(Ctx& c, const double* d_col1, const double* d_col2, uint64_t n_ro
         // resolution: shares the variance's routed cross-term buffer (same
         // slot layout), which is written only after the ranks are consumed
         out.kside = c.ws.get_t<unsigned long long>("var.xr", nslot);
-        out.sx = out.stab ? c.ws.get_t<double2>("rank.sx", nslot) : nullptr;
         launch_rank_cluster(c, plan, jobs, njobs, static_cast<uint32_t>(K), d_col1, d_col2, n_rows, out, fb, d_bad);
         std::vector<int32_t> hfb(njobs);
         PCB_CUDA(cudaMemcpyAsync(hfb.data(), fb, njobs * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));

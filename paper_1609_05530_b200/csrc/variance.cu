@@ -183,11 +183,6 @@ __global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState
             for (int j = 0; j < U; ++j) {
                 const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
                 if (i >= S.n) continue;
-                if (FAM == kGaussian && rt && R.sx) {  // slot tables: independent of the r2 gathers
-                    ta[j][0] = R.sx[c1 + (w1[j] >> 16) * R.rcap + (w1[j] & 0xffffu)];
-                    tb[j][0] = R.sx[c2 + (w2[j] >> 16) * R.rcap + (w2[j] & 0xffffu)];
-                    continue;
-                }
                 ta[j][0] = gt[2 * q1[j]];
                 tb[j][0] = gt[2 * q2[j]];
                 if (FAM == kGumbel) {
