@@ -228,8 +228,11 @@ class CopyPool {
 
   private:
     CopyPool() {
+        // the copies are host-memory-bandwidth bound: measured on a 16-core
+        // box, C5 through std::vector columns 1.56 / 2.34 / 2.68 / 2.87e9
+        // points/s with 4 / 8 / 12 / 16 threads
         unsigned hw = std::thread::hardware_concurrency();
-        unsigned n = std::max(1u, std::min(8u, hw / 2));
+        unsigned n = std::max(1u, std::min(16u, hw));
         if (const char* v = std::getenv("PCB_COPY_THREADS")) n = std::max(1, std::atoi(v));
         for (unsigned k = 1; k < n; ++k) threads_.emplace_back([this, k] { loop(k); });
     }
