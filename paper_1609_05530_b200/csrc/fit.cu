@@ -397,8 +397,11 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
 // converted at load: Frank to the edge encoding, Gumbel by rounding).
 // Four CTAs per SM: 64 registers (the allocation measured fastest; left to
 // itself the fp64 Gumbel pass takes 80 and loses 1.3 ms per family at C5).
+#ifndef PCB_LIK_OCC
+#define PCB_LIK_OCC 4
+#endif
 template <int FAM, class TI, bool F32 = (sizeof(TI) == 8)>
-__global__ void __launch_bounds__(FT, 4) k_lik(BlockState* st, const Seg* segs, int nseg, const TI* __restrict__ T,
+__global__ void __launch_bounds__(FT, PCB_LIK_OCC) k_lik(BlockState* st, const Seg* segs, int nseg, const TI* __restrict__ T,
                                            double* partials, unsigned* tickets, unsigned* running, double tol,
                                            const uint32_t* tile_list) {
     const uint32_t tile = tile_list ? tile_list[blockIdx.x] : blockIdx.x;
