@@ -61,7 +61,7 @@ constexpr double kFrank32Exact = PCB_FRANK32_EXACT;
 #endif
 constexpr double kGumbel32Exact = PCB_GUMBEL32_EXACT;
 #ifndef PCB_LIK_UNROLL
-#define PCB_LIK_UNROLL 4
+#define PCB_LIK_UNROLL 2
 #endif
 constexpr int kLikUnroll = PCB_LIK_UNROLL;  // fp64 Newton pass: points per thread in flight  // fp32 warm-up passes before the fp64 passes (fp64 mode)
 
