@@ -456,6 +456,10 @@ inline ClusterPlan plan_for(uint64_t nmax, int cl, bool lean = false) {
 }
 
 constexpr int kLeanT = 512;   // threads of a lean CTA
+#ifndef PCB_RANK_ROWMAP_DEFAULT
+#define PCB_RANK_ROWMAP_DEFAULT 1
+#endif
+constexpr int kRowMapDefault = PCB_RANK_ROWMAP_DEFAULT;
 constexpr int kLeanQ = 18;    // received elements per lean thread
 constexpr size_t kLeanSmem = 112 * 1024 - 4096;  // two per SM beside their static shared memory
 
@@ -617,7 +621,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
                                                        int32_t* fb,
                                                        int32_t* bad, int CL, uint32_t RCAP, uint32_t lg_nbl,
                                                        int tail, unsigned long long* prof, uint32_t njobs,
-                                                       uint32_t pf, unsigned long long* kside) {
+                                                       uint32_t pf, unsigned long long* kside, int rowmap) {
     namespace cg = cooperative_groups;
     constexpr int QM = LEAN ? 18 : QMAX;  // received elements per thread (RCAP <= QM * CTT)
     long long t_prev = clock64();
@@ -987,12 +991,25 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         __syncthreads();
         mark(7);
     }
+    // Element k of this thread. rowmap: warp w owns the contiguous rows
+    // [a + w*CW, a + (w+1)*CW) of the slice, 32 per step, so the per-warp
+    // send cursors hand each owner its slots in ROW order across the whole
+    // slice: the consumers' route gathers and scatters (prepare, variance
+    // passes 1 and 3) then see long runs of consecutive slots for
+    // consecutive rows (full L2 sectors), and tie runs are ordered by row like
+    // the reference's stable sort. Otherwise rows a + k*CTT + tid.
+    const uint32_t CW = 32u * ((S + CTT - 1) / CTT);
+    auto ei = [&](int k) -> uint32_t {
+        if (!rowmap) return a + k * CTT + tid;
+        const uint32_t o = static_cast<uint32_t>(k) * 32u + lane;
+        return o < CW ? a + wid * CW + o : e;
+    };
 #pragma unroll
     for (int k = 0; k < EMAX / 8; ++k) bk[k] = 0u;
     bool fin = true;
 #pragma unroll
     for (int k = 0; k < EMAX; ++k) {
-        const uint32_t i = a + k * CTT + tid;
+        const uint32_t i = ei(k);
         if (i < e) {
             const double v = xs[i];
             fin &= isfinite(v);
@@ -1003,7 +1020,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     }
 #pragma unroll
     for (int k = 0; k < EMAX; ++k)  // the counts after all the (independent) owner lookups
-        if (a + k * CTT + tid < e) atomicAdd(&s_wc[wid][(bk[k >> 3] >> ((k & 7) * 4)) & 0xfu], 1u);
+        if (ei(k) < e) atomicAdd(&s_wc[wid][(bk[k >> 3] >> ((k & 7) * 4)) & 0xfu], 1u);
     if (!__syncthreads_and(fin) && tid == 0) s_bad = 1;  // validate_data (pseudo_obs.hpp:34-36)
     if (tid < CL) {  // totals per owner, and per-warp exclusive bases
         uint32_t run = 0;
@@ -1073,7 +1090,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         unsigned long long* const kb = kside + (static_cast<uint64_t>(J.col) * K + J.seg) * CL * RCAP;
 #pragma unroll
         for (int k = 0; k < EMAX; ++k) {
-            const uint32_t i = a + k * CTT + tid;
+            const uint32_t i = ei(k);
             if (i < e) {
                 const double v = xs[i];
                 const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
@@ -1088,7 +1105,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     } else if (tail) {
 #pragma unroll
       for (int k = 0; k < EMAX; ++k) {
-        const uint32_t i = a + k * CTT + tid;
+        const uint32_t i = ei(k);
         if (i < e) {
             const unsigned long long kk = order_key(xs[i]);
             const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
@@ -1100,17 +1117,17 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     } else
 #pragma unroll
     for (int h = 0; h < EMAX; h += SB) {
-      if (a + h * CTT >= e) break;
+      if (rowmap ? (a + wid * CW + h * 32u >= e || static_cast<uint32_t>(h) * 32u >= CW) : (a + h * CTT >= e)) break;
       double xv[SB];
 #pragma unroll
       for (int k = 0; k < SB; ++k) {
-        const uint32_t i = a + (h + k) * CTT + tid;
+        const uint32_t i = ei(h + k);
         xv[k] = i < e ? x[i] : 0.0;
       }
 #pragma unroll
       for (int kk2 = 0; kk2 < SB; ++kk2) {
         const int k = h + kk2;
-        const uint32_t i = a + k * CTT + tid;
+        const uint32_t i = ei(k);
         if (i < e) {
             const unsigned long long kk = order_key(xv[kk2]);
             const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
@@ -1732,6 +1749,9 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
                             !getenv_flag("PCB_RANK_NO_TAIL")) ? 1 : 0);
     const size_t smem = fk ? fk_smem(p, lg_fk) : (tail ? std::max(p.smem, tail_bytes) : p.smem);
     const uint32_t lg_launch = fk ? lg_fk : p.lg_nbl;
+    // row-ordered receive slots (PCB_RANK_ROWMAP=0: the strided element map)
+    const char* rme = std::getenv("PCB_RANK_ROWMAP");
+    const int rowmap = (rme && rme[0] == '0') ? 0 : kRowMapDefault;
     PCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
@@ -1763,7 +1783,7 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
     }
     PCB_CUDA(cudaLaunchKernelEx(&cfg, kern, jobs, c0, c1, n_rows, out.rp, out.route, out.r2s, out.posl,
                                 out.ocnt,
-                                K, fb, bad, p.cl, p.rcap, lg_launch, tail, prof, njobs, pf, out.kside));
+                                K, fb, bad, p.cl, p.rcap, lg_launch, tail, prof, njobs, pf, out.kside, rowmap));
     if (prof) {
         unsigned long long h[12];
         PCB_CUDA(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, c.stream));
