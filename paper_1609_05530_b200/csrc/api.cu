@@ -174,6 +174,11 @@ void pipeline_blocks(pcb::Ctx& c, int fam, int prec, const double* d1, const dou
     const uint64_t K = off.size() - 1;
     RankBufs rb = rank_buffers(c, n_rows, K);
     PCB_CUDA(cudaEventRecord(c.ev[0], c.stream));
+    // Row-ordered receive slots for Frank: its variance pass 1 is bound by the
+    // scatter of the cross terms through the route, which row order turns
+    // into full L2 sectors (C5: 18.8 -> 13.7 ms); the Gaussian's route
+    // gathers measured slower with it (+4.6 ms), the Gumbel's neutral.
+    rb.r.rowmap = fam == PCB_FRANK ? 1 : 0;
     pcb::run_ranks(c, d1, d2, n_rows, off, rb.r, rb.bad);
     pcb::FitIO io;
     io.family = fam;

@@ -120,6 +120,9 @@ struct RankOut {
     uint16_t* posl = nullptr;
     uint32_t* ocnt = nullptr;
     unsigned long long* kside = nullptr;  // FK rank kernel: full order key per receive slot
+    // row-ordered receive slots (k_rank_cluster_t rowmap): set by the caller
+    // per family (-1: the default, strided)
+    int rowmap = -1;
     int cl = 0;
     uint32_t rcap = 0;
     std::vector<uint8_t> routed;  // host copy

@@ -457,7 +457,7 @@ inline ClusterPlan plan_for(uint64_t nmax, int cl, bool lean = false) {
 
 constexpr int kLeanT = 512;   // threads of a lean CTA
 #ifndef PCB_RANK_ROWMAP_DEFAULT
-#define PCB_RANK_ROWMAP_DEFAULT 1
+#define PCB_RANK_ROWMAP_DEFAULT 0
 #endif
 constexpr int kRowMapDefault = PCB_RANK_ROWMAP_DEFAULT;
 constexpr int kLeanQ = 18;    // received elements per lean thread
@@ -1749,9 +1749,10 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
                             !getenv_flag("PCB_RANK_NO_TAIL")) ? 1 : 0);
     const size_t smem = fk ? fk_smem(p, lg_fk) : (tail ? std::max(p.smem, tail_bytes) : p.smem);
     const uint32_t lg_launch = fk ? lg_fk : p.lg_nbl;
-    // row-ordered receive slots (PCB_RANK_ROWMAP=0: the strided element map)
+    // row-ordered receive slots: the caller's per-family choice (pipeline_blocks:
+    // Frank), PCB_RANK_ROWMAP=0/1 forces either map
     const char* rme = std::getenv("PCB_RANK_ROWMAP");
-    const int rowmap = (rme && rme[0] == '0') ? 0 : kRowMapDefault;
+    const int rowmap = (rme && rme[0]) ? (rme[0] == '1' ? 1 : 0) : (out.rowmap >= 0 ? out.rowmap : kRowMapDefault);
     PCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (p.cl > 8) PCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg = {};
