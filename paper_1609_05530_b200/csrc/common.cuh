@@ -96,6 +96,22 @@ constexpr int FT = 256;  // threads per tile CTA
 constexpr int PPT = 32;  // points per thread per tile
 constexpr uint32_t FTILE = FT * PPT;
 
+// Row of a tile handled by this thread at step k of the route-gathering /
+// scattering passes (prepare, variance passes 1 and 3). PCB_WARP_CHUNK: each
+// warp walks its own contiguous FTILE/8 rows, so the 8 warps of a tile touch
+// 8 distant slot runs of the rank stage's route instead of the same ones;
+// otherwise the tile's threads cover FT consecutive rows per step.
+#ifndef PCB_WARP_CHUNK
+#define PCB_WARP_CHUNK 0
+#endif
+__device__ __forceinline__ uint32_t tile_row(uint32_t k) {
+#if PCB_WARP_CHUNK
+    return (threadIdx.x >> 5) * (FTILE / (FT / 32)) + k * 32u + (threadIdx.x & 31u);
+#else
+    return k * FT + threadIdx.x;
+#endif
+}
+
 // Stores this tile's NV partial sums; the segment's last-arriving tile sums
 // all the segment's tile partials in tile order (deterministic: fixed
 // per-tile trees, fixed final order, no floating-point atomics). Returns

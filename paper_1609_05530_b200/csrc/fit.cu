@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
         if (!u1) {
 #pragma unroll
             for (int j = 0; j < U; ++j) {
-                const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+                const uint32_t i = base + tile_row(k0 + j);
                 if (i < S.n) {
                     const uint64_t row = S.begin + i;
                     if (rt) {
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
             if (rt) {
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
-                    const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+                    const uint32_t i = base + tile_row(k0 + j);
                     if (i < S.n) {
                         ra[j] = R.r2s[slot_index(R, nseg, 0, m, ra[j])];
                         rb[j] = R.r2s[slot_index(R, nseg, 1, m, rb[j])];
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
         }
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            const uint32_t i = base + tile_row(k0 + j);
             if (i < S.n) {
                 const uint64_t row = S.begin + i;
                 if (u1) {
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(FT, PCB_PREP_OCC) k_prepare(BlockState* st, co
         }
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            const uint32_t i = base + tile_row(k0 + j);
             if (i >= S.n) continue;
             const uint64_t row = S.begin + i;
             const double u = clamp_unit(uu[j]), w = clamp_unit(ww[j]);

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState
         double uu[U], ww[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            const uint32_t i = base + tile_row(k0 + j);
             if (i < S.n) {
                 const uint64_t row = S.begin + i;
                 if (rt) {
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState
         }
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            const uint32_t i = base + tile_row(k0 + j);
             if (i >= S.n) continue;
             if (!rt) {
                 q1[j] = rank_r2(p1[j]);
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState
         if constexpr (MODE == kFromTable) {
 #pragma unroll
             for (int j = 0; j < U; ++j) {
-                const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+                const uint32_t i = base + tile_row(k0 + j);
                 if (i >= S.n) continue;
                 ta[j][0] = gt[2 * q1[j]];
                 tb[j][0] = gt[2 * q2[j]];
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(FT, VarOcc<FAM>::value) k_var_point(BlockState
         }
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            const uint32_t i = base + tile_row(k0 + j);
             if (i >= S.n) continue;
             const uint64_t row = S.begin + i;
             double u, w;
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(FT, PCB_FINAL_OCC) k_var_final(BlockState* st,
         double zz[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            const uint32_t i = base + tile_row(k0 + j);
             if (i < S.n) {
                 const uint64_t row = S.begin + i;
                 r1[j] = route[row];
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(FT, PCB_FINAL_OCC) k_var_final(BlockState* st,
         double w1[U], w2[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            const uint32_t i = base + tile_row(k0 + j);
             if (i < S.n) {
                 w1[j] = x1[(r1[j] >> 16) * RCAP + (r1[j] & 0xffffu)] + k1[r1[j] >> 16];
                 w2[j] = x2[(r2[j] >> 16) * RCAP + (r2[j] & 0xffffu)] + k2[r2[j] >> 16];
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(FT, PCB_FINAL_OCC) k_var_final(BlockState* st,
         }
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const uint32_t i = base + (k0 + j) * FT + threadIdx.x;
+            const uint32_t i = base + tile_row(k0 + j);
             if (i < S.n) {
                 double z = zz[j];
                 z += (w1[j] - cj1) * inv_n;
