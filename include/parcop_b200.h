@@ -173,8 +173,11 @@ int pcb_combine(pcb_context* ctx, const pcb_fit_result* results, uint64_t n_bloc
                 pcb_combined* out);
 
 /* One shard of fit_parallel: raw columns -> per-block ranks -> fit ->
- * variance, no combine. A multi-GPU caller gives each GPU a contiguous
- * range of blocks, gathers the records, and calls pcb_combine. */
+ * variance, no combine. With a pcb_create_multi context the blocks are
+ * sharded over its devices and the records gathered here; a one-process-
+ * per-GPU caller instead gives each process a contiguous range of blocks,
+ * all-gathers the records, and calls pcb_combine. Host columns may be pinned
+ * or pageable (streamed in block groups while earlier groups compute). */
 int pcb_fit_blocks(pcb_context* ctx, int family, int precision, const double* col1, const double* col2,
                    uint64_t n_rows, const uint64_t* seg_offsets, uint64_t n_seg, pcb_fit_result* out);
 
