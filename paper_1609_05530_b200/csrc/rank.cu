@@ -410,6 +410,9 @@ uint32_t tiles_of(uint64_t n) { return static_cast<uint32_t>((n + RTILE - 1) / R
 // skewed data) or
 // a non-finite range falls back to the global path.
 constexpr int CT = 1024;  // threads per cluster CTA
+#ifndef PCB_RANK_DBL
+#define PCB_RANK_DBL 1
+#endif
 constexpr int EMAX = 16;         // slice elements per thread (slice <= 16K)
 constexpr int QMAX = 16;         // received elements per thread (RCAP <= QMAX * CT)
 constexpr int kMaxCluster = 16;
@@ -624,6 +627,12 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
                                                        uint32_t pf, unsigned long long* kside, int rowmap) {
     namespace cg = cooperative_groups;
     constexpr int QM = LEAN ? 18 : QMAX;  // received elements per thread (RCAP <= QM * CTT)
+    // DBL: the receive buffer holds the values themselves (-0 canonicalised to
+    // +0 by adding +0.0) instead of their order keys. Every value reaching it
+    // is finite (validate_data runs before the send), so double comparisons
+    // order them exactly as the keys do (one DSETP instead of two 32-bit
+    // compares each for < and ==), and the owner's bucket needs no key_value.
+    constexpr bool DBL = PCB_RANK_DBL && !QUANT && !FK && !LEAN;
     long long t_prev = clock64();
     auto mark = [&](int k) {  // optional phase timing (PCB_RANK_PROFILE): thread 0's clock deltas
         if (prof && threadIdx.x == 0) {
@@ -644,6 +653,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
 
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* recv_key = reinterpret_cast<unsigned long long*>(smem);
+    const double* const recv_dbl = reinterpret_cast<const double*>(smem);  // DBL: the same slots as values
     // FK: [fine keys, 4 B per slot | region B: the staged slice, after the send outw / lhs / perm]
     uint32_t* const recv_fk = reinterpret_cast<uint32_t*>(smem);
     unsigned char* const regB = smem + ((static_cast<size_t>(RCAP) * 4 + 15) & ~static_cast<size_t>(15));
@@ -1107,7 +1117,8 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
       for (int k = 0; k < EMAX; ++k) {
         const uint32_t i = ei(k);
         if (i < e) {
-            const unsigned long long kk = order_key(xs[i]);
+            const unsigned long long kk = DBL ? static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(xs[i], 0.0)))
+                                              : order_key(xs[i]);
             const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
             const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
             route_j[i] = (d << 16) | slot;
@@ -1129,7 +1140,8 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
         const int k = h + kk2;
         const uint32_t i = ei(k);
         if (i < e) {
-            const unsigned long long kk = order_key(xv[kk2]);
+            const unsigned long long kk = DBL ? static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(xv[kk2], 0.0)))
+                                              : order_key(xv[kk2]);
             const uint32_t d = (bk[k >> 3] >> ((k & 7) * 4)) & 0xfu;
             const uint32_t slot = atomicAdd(&s_wc[wid][d], 1u);
             route_j[i] = (d << 16) | slot;
@@ -1197,7 +1209,9 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
                     if (j0 + u * CTT < T) outw[j0 + u * CTT] = lv[u];
             }
         for (uint32_t j = tid; j < T; j += CTT) {
-            const uint32_t lb = qmode ? outw[j] : (cbucket(recv_key[j], hm, scale, nbtot) & lmask);
+            const uint32_t lb = qmode ? outw[j]
+                                      : ((DBL ? cbucket_v(recv_dbl[j], hm, scale, nbtot) : cbucket(recv_key[j], hm, scale, nbtot)) &
+                                         lmask);
             const uint32_t sh = (lb & 1) * 16;
             const uint32_t idx = (atomicAdd(lhw + (lb >> 1), 1u << sh) >> sh) & 0xffffu;
             outw[j] = lb | (idx << 14);
@@ -1251,6 +1265,27 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
                     }
                 }
             }
+            const uint32_t llt = s0 + less;
+            outw[j] = ((2u * llt + same + 1u) << 16) | (llt + before) | (before == 0 ? 0x8000u : 0u);
+        }
+    } else if constexpr (DBL) {
+#pragma unroll
+        for (int k = 0; k < QM; ++k) {
+            const uint32_t qq = tid + k * CTT;
+            if (qq >= T) break;
+            const uint32_t j = perm[qq];
+            const double kv = recv_dbl[j];
+            const uint32_t lb = outw[j] & 0x3fffu;
+            const uint32_t s0 = lhs[lb], s1 = lhs[lb + 1];
+            uint32_t less = 0, sb = 0;  // sb = same | before << 16
+#pragma unroll 2
+            for (uint32_t q = s0; q < s1; ++q) {
+                const uint32_t o = perm[q];
+                const double kq = recv_dbl[o];
+                less += kq < kv;
+                if (kq == kv) sb += 1u + (static_cast<uint32_t>(o < j) << 16);
+            }
+            const uint32_t same = sb & 0xffffu, before = sb >> 16;
             const uint32_t llt = s0 + less;
             outw[j] = ((2u * llt + same + 1u) << 16) | (llt + before) | (before == 0 ? 0x8000u : 0u);
         }
