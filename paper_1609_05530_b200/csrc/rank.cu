@@ -82,7 +82,7 @@ __device__ __forceinline__ int range_of_tile(const RankRange* rr, int nr, uint32
 
 template <bool L0>
 __device__ __forceinline__ void load_elem(const RankRange& R, uint32_t i, const double* c0, const double* c1,
-                                          const unsigned long long* skey, const uint32_t* sidx,
+                                          const ulonglong2* srec,
                                           unsigned long long& key, uint32_t& idx, bool& finite) {
     if (L0) {
         const double x = __ldg((R.col ? c1 : c0) + R.src_base + i);
@@ -90,8 +90,9 @@ __device__ __forceinline__ void load_elem(const RankRange& R, uint32_t i, const 
         key = order_key(x);
         idx = i;
     } else {
-        key = skey[R.src_base + i];
-        idx = sidx[R.src_base + i];
+        const ulonglong2 rec = srec[R.src_base + i];
+        key = rec.x;
+        idx = static_cast<uint32_t>(rec.y);
         finite = true;
     }
 }
@@ -108,7 +109,7 @@ __device__ __forceinline__ uint32_t bucket_of(const RankRange& R, unsigned long 
 
 template <bool L0>
 __global__ void __launch_bounds__(RT) k_minmax(RankRange* rr, int nr, const double* c0, const double* c1,
-                                              const unsigned long long* skey, const uint32_t* sidx, int32_t* bad) {
+                                              const ulonglong2* srec, int32_t* bad) {
     const int r = range_of_tile(rr, nr, blockIdx.x);
     const RankRange R = rr[r];
     const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(RT) k_minmax(RankRange* rr, int nr, const doub
         unsigned long long k;
         uint32_t id;
         bool fin;
-        load_elem<L0>(R, i, c0, c1, skey, sidx, k, id, fin);
+        load_elem<L0>(R, i, c0, c1, srec, k, id, fin);
         allfin &= fin;
         kmn = min(kmn, k);
         kmx = max(kmx, k);
@@ -207,7 +208,7 @@ __global__ void k_resolve(RankRange* rr, int nr, int level0) {
 
 template <bool L0>
 __global__ void __launch_bounds__(RT) k_hist(const RankRange* rr, int nr, const double* c0, const double* c1,
-                                            const unsigned long long* skey, const uint32_t* sidx, uint32_t* hist) {
+                                            const ulonglong2* srec, uint32_t* hist) {
     const int r = range_of_tile(rr, nr, blockIdx.x);
     const RankRange R = rr[r];
     const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(RT) k_hist(const RankRange* rr, int nr, const 
         unsigned long long k;
         uint32_t id;
         bool fin;
-        load_elem<L0>(R, i, c0, c1, skey, sidx, k, id, fin);
+        load_elem<L0>(R, i, c0, c1, srec, k, id, fin);
         atomicAdd(hist + R.bbase + bucket_of(R, k, id), 1u);
     }
 }
@@ -309,56 +310,69 @@ __global__ void __launch_bounds__(1024) k_scan_apply(const RankRange* rr, const 
 
 template <bool L0>
 __global__ void __launch_bounds__(RT) k_scatter(const RankRange* rr, int nr, const double* c0, const double* c1,
-                                               const unsigned long long* skey, const uint32_t* sidx,
-                                               uint32_t* cursor, unsigned long long* dkey, uint32_t* didx) {
+                                               const ulonglong2* srec, uint32_t* cursor, ulonglong2* drec) {
+    // (key, index) records of 16 bytes: one scattered store per element (a
+    // partial-sector write to a random address is the cost of this pass);
+    // SU elements per thread in flight
+    constexpr int SU = 4;
     const int r = range_of_tile(rr, nr, blockIdx.x);
     const RankRange R = rr[r];
     const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
     const uint32_t end = min(begin + RTILE, R.n);
-    for (uint32_t i = begin + threadIdx.x; i < end; i += RT) {
-        unsigned long long k;
-        uint32_t id;
-        bool fin;
-        load_elem<L0>(R, i, c0, c1, skey, sidx, k, id, fin);
-        const uint32_t slot = atomicAdd(cursor + R.bbase + bucket_of(R, k, id), 1u);
-        dkey[R.dst_base + slot] = k;
-        didx[R.dst_base + slot] = id;
+    for (uint32_t i0 = begin + threadIdx.x; i0 < end; i0 += SU * RT) {
+        unsigned long long k[SU];
+        uint32_t id[SU], slot[SU];
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+            const uint32_t i = i0 + u * RT;
+            if (i < end) {
+                bool fin;
+                load_elem<L0>(R, i, c0, c1, srec, k[u], id[u], fin);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < SU; ++u)
+            if (i0 + u * RT < end) slot[u] = atomicAdd(cursor + R.bbase + bucket_of(R, k[u], id[u]), 1u);
+#pragma unroll
+        for (int u = 0; u < SU; ++u)
+            if (i0 + u * RT < end) drec[R.dst_base + slot[u]] = make_ulonglong2(k[u], id[u]);
     }
 }
 
 // One thread per element of the scattered range; buckets <= CAP are ranked
 // by counting inside the bucket (L1-resident neighbours).
-__global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const unsigned long long* dkey,
-                                            const uint32_t* didx, const uint32_t* hist, const uint32_t* bstart,
+__global__ void __launch_bounds__(RT) k_rank(const RankRange* rr, int nr, const ulonglong2* drec,
+                                            const uint32_t* hist, const uint32_t* bstart,
                                             uint64_t n_rows, unsigned long long* o_rp) {
     const int r = range_of_tile(rr, nr, blockIdx.x);
     const RankRange R = rr[r];
     const uint32_t begin = (blockIdx.x - R.tile0) * RTILE;
     const uint32_t end = min(begin + RTILE, R.n);
     for (uint32_t p = begin + threadIdx.x; p < end; p += RT) {
-        const unsigned long long k = dkey[R.dst_base + p];
-        const uint32_t id = didx[R.dst_base + p];
+        const ulonglong2 me = drec[R.dst_base + p];
+        const unsigned long long k = me.x;
+        const uint32_t id = static_cast<uint32_t>(me.y);
         const uint32_t b = bucket_of(R, k, id);
         const uint32_t cnt = hist[R.bbase + b];
         if (cnt > CAP) continue;  // refined at the next level
         const uint32_t s = bstart[R.bbase + b];
-        const unsigned long long* bk = dkey + R.dst_base + s;
-        const uint32_t* bi = didx + R.dst_base + s;
+        const ulonglong2* br = drec + R.dst_base + s;
         uint32_t lt, eq, pos;
         if (R.mode == 2) {
             uint32_t before = 0;
-            for (uint32_t q = 0; q < cnt; ++q) before += bi[q] < id;
+            for (uint32_t q = 0; q < cnt; ++q) before += static_cast<uint32_t>(br[q].y) < id;
             lt = R.run_start;
             eq = R.run_len;
             pos = R.lt_base + s + before;
         } else {
             uint32_t less = 0, same = 0, before = 0;
             for (uint32_t q = 0; q < cnt; ++q) {
-                const unsigned long long kq = bk[q];
+                const ulonglong2 rq = br[q];
+                const unsigned long long kq = rq.x;
                 less += kq < k;
                 const bool e = kq == k;
                 same += e;
-                before += e && (bi[q] < id);
+                before += e && (static_cast<uint32_t>(rq.y) < id);
             }
             lt = R.lt_base + s + less;
             eq = same;
@@ -1876,8 +1890,7 @@ void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64
     }
     if (ranges.empty()) return;
     const uint64_t total = 2 * n_rows;
-    auto* keyA = c.ws.get_t<unsigned long long>("rank.keyA", total);
-    auto* idxA = c.ws.get_t<uint32_t>("rank.idxA", total);
+    auto* recA = c.ws.get_t<ulonglong2>("rank.recA", total);
     const uint32_t ov_cap = static_cast<uint32_t>(total / CAP + 16);
     auto* ov = c.ws.get_t<Oversize>("rank.ov", ov_cap);
     auto* ovn = c.ws.get_t<uint32_t>("rank.ovn", 1);
@@ -1888,16 +1901,15 @@ void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64
     auto* cursor = c.ws.get_t<uint32_t>("rank.cursor", bsum);
     auto* h_ovn = static_cast<uint32_t*>(c.host_staging(sizeof(uint32_t)));
 
-    auto run_level = [&](bool l0, const unsigned long long* skey, const uint32_t* sidx, unsigned long long* dkey,
-                         uint32_t* didx, uint64_t nbuckets, uint32_t ntiles) {
+    auto run_level = [&](bool l0, const ulonglong2* srec, ulonglong2* drec, uint64_t nbuckets, uint32_t ntiles) {
         PCB_CUDA(cudaMemcpyAsync(d_rr, ranges.data(), ranges.size() * sizeof(RankRange), cudaMemcpyHostToDevice, st));
         PCB_CUDA(cudaMemsetAsync(hist, 0, nbuckets * sizeof(uint32_t), st));
         PCB_CUDA(cudaMemsetAsync(ovn, 0, sizeof(uint32_t), st));
-        if (l0) k_minmax<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, d_bad);
-        else k_minmax<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, d_bad);
+        if (l0) k_minmax<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, srec, d_bad);
+        else k_minmax<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, srec, d_bad);
         k_resolve<<<(nr + 127) / 128, 128, 0, st>>>(d_rr, nr, l0 ? 1 : 0);
-        if (l0) k_hist<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, hist);
-        else k_hist<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, hist);
+        if (l0) k_hist<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, srec, hist);
+        else k_hist<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, srec, hist);
         {  // chunked bucket scan
             std::vector<ScanChunk> hc;
             std::vector<uint32_t> c0(ranges.size() + 1);
@@ -1918,19 +1930,18 @@ void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64
             k_scan_apply<<<nch, 1024, 0, st>>>(d_rr, d_ch, hist, coff, bstart, cursor, ov, ovn, ov_cap);
             c.count_launch(2);
         }
-        if (l0) k_scatter<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
-        else k_scatter<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, skey, sidx, cursor, dkey, didx);
-        k_rank<<<ntiles, RT, 0, st>>>(d_rr, nr, dkey, didx, hist, bstart, n_rows, out.rp);
+        if (l0) k_scatter<true><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, srec, cursor, drec);
+        else k_scatter<false><<<ntiles, RT, 0, st>>>(d_rr, nr, d_col1, d_col2, srec, cursor, drec);
+        k_rank<<<ntiles, RT, 0, st>>>(d_rr, nr, drec, hist, bstart, n_rows, out.rp);
         c.count_launch(6);
         PCB_CUDA(cudaMemcpyAsync(h_ovn, ovn, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         PCB_CUDA(cudaStreamSynchronize(st));
         return *h_ovn;
     };
 
-    uint32_t n_ov = run_level(true, nullptr, nullptr, keyA, idxA, bsum, tiles);
+    uint32_t n_ov = run_level(true, nullptr, recA, bsum, tiles);
     // ---- refinement levels (adversarial / heavily skewed inputs only)
-    unsigned long long *cur_key = keyA, *nxt_key = nullptr;
-    uint32_t *cur_idx = idxA, *nxt_idx = nullptr;
+    ulonglong2 *cur_rec = recA, *nxt_rec = nullptr;
     int level = 0;
     while (n_ov > 0) {
         if (++level > 80) throw Error(5, "rank refinement did not terminate");
@@ -1940,10 +1951,7 @@ void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64
         PCB_CUDA(cudaMemcpyAsync(hov.data(), ov, n_ov * sizeof(Oversize), cudaMemcpyDeviceToHost, st));
         PCB_CUDA(cudaMemcpyAsync(parents.data(), d_rr, parents.size() * sizeof(RankRange), cudaMemcpyDeviceToHost, st));
         PCB_CUDA(cudaStreamSynchronize(st));
-        if (!nxt_key) {
-            nxt_key = c.ws.get_t<unsigned long long>("rank.keyB", total);
-            nxt_idx = c.ws.get_t<uint32_t>("rank.idxB", total);
-        }
+        if (!nxt_rec) nxt_rec = c.ws.get_t<ulonglong2>("rank.recB", total);
         ranges.clear();
         bsum = 0;
         tiles = 0;
@@ -1977,9 +1985,8 @@ void run_ranks_global(Ctx& c, const double* d_col1, const double* d_col2, uint64
         hist = c.ws.get_t<uint32_t>("rank.hist", bsum);
         bstart = c.ws.get_t<uint32_t>("rank.bstart", bsum);
         cursor = c.ws.get_t<uint32_t>("rank.cursor", bsum);
-        n_ov = run_level(false, cur_key, cur_idx, nxt_key, nxt_idx, bsum, tiles);
-        std::swap(cur_key, nxt_key);
-        std::swap(cur_idx, nxt_idx);
+        n_ov = run_level(false, cur_rec, nxt_rec, bsum, tiles);
+        std::swap(cur_rec, nxt_rec);
     }
 }
 
