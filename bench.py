@@ -375,6 +375,16 @@ def run_ours(args):
         fp64_db = json.load(open(os.path.join(ROOT, "profiles", "r02_fp64_pipe.json")))["kernels"]
     except Exception:
         fp64_db = {}
+    # instruction issue: the rank kernel is issue / shared-memory bound, not HBM bound:
+    # measured warp instructions per point (profiles/issue.json) x points / live ms against the
+    # issue peak (SMs x 4 schedulers x the SM clock sampled during the timed region)
+    issue_db = {}
+    try:
+        issue_db = json.load(open(os.path.join(ROOT, "profiles", "issue.json")))
+    except Exception:
+        issue_db = {}
+    sm_hz = float((clk or {}).get("sm_mhz") or 1965.0) * 1e6
+    issue_peak = torch.cuda.get_device_properties(local).multi_processor_count * 4 * sm_hz
     l2_sect = {}  # kernel -> sectors per step
     per_kernel = {}  # name -> [ms, launches, bytes, fp64 instr (frozen F), fp64 instr (measured per point)]
     def add(name, ms, launches, nbytes, instr, fam_name, per_launch=False, units=0.0):
@@ -426,6 +436,12 @@ def run_ours(args):
                 "frac_by_frozen_F": instr / (kms * 1e-3) / fp64_peak,
                 "source": "ncu DFMA+DADD+DMUL per point (profiles/r02_fp64_pipe.json) x live ms",
                 "pipe_active_pct": {f: v.get("sm__pipe_fp64_cycles_active_pct") for f, v in fp64_db.get(kname, {}).items()}}
+        if isinstance(issue_db.get(kname), (int, float)):
+            ips = issue_db[kname] * rows * nl / (kms * 1e-3)
+            table[kname]["issue"] = {"warp_instr_per_s": ips, "peak_warp_instr_per_s": issue_peak,
+                                     "frac": ips / issue_peak,
+                                     "source": "profiles/issue.json (ncu smsp__inst_executed per point) x live ms; "
+                                               "peak = SMs x 4 schedulers x sampled SM clock"}
         if kname in l2_sect and l2_rate:
             rate = l2_sect[kname] / (kms * 1e-3)
             table[kname]["l2"] = {"sectors_per_s": rate, "peak_random_sectors_per_s": l2_rate,
@@ -441,6 +457,7 @@ def run_ours(args):
                 "traffic": (traffic_db[dom] * rows if dom in traffic_db else None),
                 "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/r02_ncu_full.md, per point x points)",
                 "algorithmic_bytes_per_launch": per_kernel[dom][2] / max(per_kernel[dom][1], 1),
+                "issue": tk.get("issue"),
                 "per_kernel": table}
         # SURVEY.md §8(d) pipeline roofline per GPU (B_pipe = 96 B/pt against HBM; F_pipe with the
         # oracle's mean Newton passes against FP64): the step's floor for the C5 mix
