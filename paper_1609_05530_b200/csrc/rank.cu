@@ -794,6 +794,7 @@ __global__ void __launch_bounds__(CTT, LEAN ? 2 : 1) k_rank_cluster_t(const Clus
     if (tid == 0) s_bad = 0;
     for (int q = tid; q < (CTT / 32) * kMaxCluster; q += CTT) (&s_wc[0][0])[q] = 0u;
     cta_extremes();
+    mark(11);
     cluster.sync();
     mark(0);
     cluster_extremes();
@@ -1476,6 +1477,7 @@ __global__ void __launch_bounds__(CT2, 2) k_rank_fk2(const ClusterJob* jobs, con
     if (tid == 0) s_bad = 0;
     for (int q = tid; q < (CT2 / 32) * kMaxCluster; q += CT2) (&s_wc[0][0])[q] = 0u;
     cta_extremes();
+    mark(11);
     cluster.sync();
     mark(0);
     cluster_extremes();
@@ -1841,8 +1843,8 @@ void launch_rank_cluster(Ctx& c, const ClusterPlan& p, const ClusterJob* jobs, u
         const double ctas = static_cast<double>(njobs) * p.cl;
         std::fprintf(stderr, "[rank profile%s%s] CL=%d S=%u lean=%d: cycles/CTA  minmax %.0f  count %.0f  matrix %.0f  "
                      "send %.0f  localsort %.0f  rank %.0f  qsample+sort %.0f  qhist-loop %.0f  qhist-sync %.0f  qcum %.0f  "
-                     "qshare %.0f\n", quant ? " quantile" : "", fk ? " fk" : "", p.cl, p.s, int(p.lean), h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
-                     h[4] / ctas, h[5] / ctas, h[6] / ctas, h[8] / ctas, h[9] / ctas, h[10] / ctas, h[7] / ctas);
+                     "qshare %.0f  [pre-barrier %.0f]\n", quant ? " quantile" : "", fk ? " fk" : "", p.cl, p.s, int(p.lean), h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
+                     h[4] / ctas, h[5] / ctas, h[6] / ctas, h[8] / ctas, h[9] / ctas, h[10] / ctas, h[7] / ctas, h[11] / ctas);
     }
     c.count_launch();
 }
