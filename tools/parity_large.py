@@ -12,6 +12,10 @@
 
     python tools/parity_large.py c5 [--picks N] [--out profiles/r02_parity_c5.json]
     python tools/parity_large.py c4 [--n 100000000] [--out profiles/r02_parity_c4.json]
+    python tools/parity_large.py configs [--out profiles/r02_parity_configs.json]
+        every block of BASELINE configs[0..2] (C1 Gaussian 0.5 n=1e4 K=10, C2
+        Frank 5 n=1e6 K=100, C3 Gumbel 2 n=1e8 K=1000) and of the fp64 C4 grid
+        (3 families x 3 theta x K in {10, 100, 1000, 10000} at n=1e8)
 
 The oracle is test infrastructure (oracle/): this script is a checker, run on
 the GPU box; tests/test_gpu_large.py runs the same functions at bounded size.
@@ -187,7 +191,7 @@ def c4_case(ctx, orc, fam, theta, n, K, workers=None, rank_workers=None):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["c5", "c4"])
+    ap.add_argument("which", choices=["c5", "c4", "configs"])
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--picks", type=int, default=None, help="C5: blocks per family spread over the range (default all)")
     ap.add_argument("--families", default="0,1,2")
@@ -206,6 +210,19 @@ def main():
             picks = None if args.picks is None else np.linspace(0, 7999, args.picks).round().astype(np.int64)
             r = c5_family(ctx, orc, fam, th, n=n, picks=picks)
             r["name"] = name
+            print(json.dumps(r), flush=True)
+            out.append(r)
+    elif args.which == "configs":
+        cases = [("C1", 0, 0.5, 10_000, 10), ("C2", 1, 5.0, 1_000_000, 100), ("C3", 2, 2.0, 100_000_000, 1000)]
+        for fam, ths in ((0, (0.2, 0.5, 0.8)), (1, (2.0, 5.0, 10.0)), (2, (1.5, 2.0, 3.0))):
+            for th in ths:
+                for K in (10, 100, 1000, 10000):
+                    cases.append(("C4", fam, th, 100_000_000, K))
+        for cfg, fam, th, n, K in cases:
+            if str(fam) not in args.families.split(","):
+                continue
+            r = c5_family(ctx, orc, fam, th, n=n, K=K)
+            r["name"] = cfg
             print(json.dumps(r), flush=True)
             out.append(r)
     else:
