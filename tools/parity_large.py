@@ -12,7 +12,7 @@
 
     python tools/parity_large.py c5 [--picks N] [--out profiles/r02_parity_c5.json]
     python tools/parity_large.py c4 [--n 100000000] [--out profiles/r02_parity_c4.json]
-    python tools/parity_large.py configs [--out profiles/r02_parity_configs.json]
+    python tools/parity_large.py configs [--fp32] [--out profiles/r02_parity_configs.json]
         every block of BASELINE configs[0..2] (C1 Gaussian 0.5 n=1e4 K=10, C2
         Frank 5 n=1e6 K=100, C3 Gumbel 2 n=1e8 K=1000) and of the fp64 C4 grid
         (3 families x 3 theta x K in {10, 100, 1000, 10000} at n=1e8)
@@ -54,14 +54,14 @@ def _recs_np(recs):
     return th, s2, ll, cv
 
 
-def _device_records(ctx, fam, c1, c2, n, off):
+def _device_records(ctx, fam, c1, c2, n, off, precision=0):
     """pcb_fit_blocks over device columns -> host structured records."""
     import torch
     from paper_1609_05530_b200 import _lib as L
     k = len(off) - 1
     rec = torch.zeros((k, 6), dtype=torch.int64, device=c1.device)
     offc = np.ascontiguousarray(off, np.uint64)
-    ctx.check(ctx.lib.pcb_fit_blocks(ctx.ptr, fam, 0, c1.data_ptr(), c2.data_ptr(), n,
+    ctx.check(ctx.lib.pcb_fit_blocks(ctx.ptr, fam, precision, c1.data_ptr(), c2.data_ptr(), n,
                                      offc.ctypes.data_as(C.POINTER(C.c_uint64)), k, rec.data_ptr()))
     torch.cuda.synchronize()
     arr = rec.cpu().numpy()
@@ -82,8 +82,9 @@ def _compare(dev, cpu):
     return r
 
 
-def c5_family(ctx, orc, fam, theta, n=1_000_000_000, K=8000, picks=None, chunk=400, workers=None):
-    """All K blocks on device; the oracle re-fits `picks` (all if None)."""
+def c5_family(ctx, orc, fam, theta, n=1_000_000_000, K=8000, picks=None, chunk=400, workers=None, precision=0):
+    """All K blocks on device; the oracle re-fits `picks` (all if None).
+    precision 1: the device's fp32 likelihood path, held to 1e-5."""
     import torch
     import paper_1609_05530_b200 as pcb
     workers = workers or os.cpu_count() or 1
@@ -92,7 +93,7 @@ def c5_family(ctx, orc, fam, theta, n=1_000_000_000, K=8000, picks=None, chunk=4
     off[-1] = n
     X = pcb.sample_matrix(fam, theta, n, K, base_seed=BASE_SEED, device_out=True, ctx=ctx)
     t0 = time.perf_counter()
-    dev = _device_records(ctx, fam, X.col1, X.col2, n, off)
+    dev = _device_records(ctx, fam, X.col1, X.col2, n, off, precision)
     t_dev = time.perf_counter() - t0
     sel = np.arange(K) if picks is None else np.unique(np.asarray(picks, np.int64))
     cpu = []
@@ -125,8 +126,11 @@ def c5_family(ctx, orc, fam, theta, n=1_000_000_000, K=8000, picks=None, chunk=4
         tall = (L.FitResultC * K)(*dev)
         ctx.check(ctx.lib.pcb_combine(ctx.ptr, C.addressof(tall), K, None, C.byref(comb)))
         res["theta_combined_device_all_blocks"] = comb.theta_combined
-    res["ok"] = bool(res["converged_mismatch"] == 0 and res["max_rel_theta"] <= TOL and
-                     res["max_rel_sigma2"] <= TOL and res["rel_theta_combined"] <= TOL and
+    tol = 1e-5 if precision else TOL
+    res["precision"] = "fp32" if precision else "fp64"
+    res["tol"] = tol
+    res["ok"] = bool(res["converged_mismatch"] == 0 and res["max_rel_theta"] <= tol and
+                     res["max_rel_sigma2"] <= tol and res["rel_theta_combined"] <= tol and
                      res["blocks_used_device"] == res["blocks_used_oracle"])
     del X
     torch.cuda.empty_cache()
@@ -147,7 +151,7 @@ def c4_case(ctx, orc, fam, theta, n, K, workers=None, rank_workers=None):
     X = pcb.sample_matrix(fam, theta, n, 1000, base_seed=BASE_SEED, device_out=True, ctx=ctx)
     off = orc.partition(n, K)
     t0 = time.perf_counter()
-    dev = _device_records(ctx, fam, X.col1, X.col2, n, off)
+    dev = _device_records(ctx, fam, X.col1, X.col2, n, off, precision)
     t_dev = time.perf_counter() - t0
     U = pcb.normalized_ranks(X, off, ctx=ctx)
     h1, h2 = X.col1.cpu().numpy(), X.col2.cpu().numpy()
@@ -197,6 +201,7 @@ def main():
     ap.add_argument("--families", default="0,1,2")
     ap.add_argument("--ks", default="10,1")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--fp32", action="store_true", help="configs: the fp32 likelihood path (bar 1e-5)")
     args = ap.parse_args()
     import paper_1609_05530_b200 as pcb
     from oracle.oracle import oracle_lib
@@ -221,7 +226,7 @@ def main():
         for cfg, fam, th, n, K in cases:
             if str(fam) not in args.families.split(","):
                 continue
-            r = c5_family(ctx, orc, fam, th, n=n, K=K)
+            r = c5_family(ctx, orc, fam, th, n=n, K=K, precision=1 if args.fp32 else 0)
             r["name"] = cfg
             print(json.dumps(r), flush=True)
             out.append(r)
