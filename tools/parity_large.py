@@ -151,7 +151,7 @@ def c4_case(ctx, orc, fam, theta, n, K, workers=None, rank_workers=None):
     X = pcb.sample_matrix(fam, theta, n, 1000, base_seed=BASE_SEED, device_out=True, ctx=ctx)
     off = orc.partition(n, K)
     t0 = time.perf_counter()
-    dev = _device_records(ctx, fam, X.col1, X.col2, n, off, precision)
+    dev = _device_records(ctx, fam, X.col1, X.col2, n, off)
     t_dev = time.perf_counter() - t0
     U = pcb.normalized_ranks(X, off, ctx=ctx)
     h1, h2 = X.col1.cpu().numpy(), X.col2.cpu().numpy()
